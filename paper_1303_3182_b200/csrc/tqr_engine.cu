@@ -1,0 +1,534 @@
+// Tiled QR engine: persistent dataflow executor, tile pack/unpack, FP64
+// peak probe, and the C-ABI numeric entry points of include/tqr.h.
+//
+// The elimination list is compiled once (tqr_plan_create) into a static
+// device schedule: every kernel of the reference trace (qr.py:376-532)
+// becomes one work item (panels) or nb/64 column-slab items (updates); the
+// reference hazard DAG (taskgraph.py:262-322) is refined to slab
+// granularity and stored as per-item predecessor lists; items are ordered
+// by weighted ASAP start (a topological order).  One persistent kernel with
+// one 256-thread CTA per SM dequeues items in that order, waits on its
+// predecessors' done flags (acquire), runs the kernel, and publishes its own
+// flag (release).  No host round-trips per task.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <map>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "capi_internal.hpp"
+#include "tqr_tasks.cuh"
+
+using namespace tqrk;
+
+namespace {
+
+struct Item {
+  int8_t kind;
+  int8_t slab;
+  int16_t pad;
+  int32_t i, piv, k, j;
+  int32_t pred_lo, pred_n;
+};
+static_assert(sizeof(Item) == 28, "item layout");
+
+struct ExecParams {
+  const Item* items;
+  const int32_t* preds;
+  int n_items;
+  int* done;
+  int* queue;
+  const double* vtiles;  // reflector source (factored tiles)
+  double* tiles;         // tiles the items write (== vtiles when factoring)
+  double* tg;
+  double* te;
+  int p;
+};
+
+template <int NB>
+__device__ __forceinline__ size_t toff(int p, int i, int j) {
+  return (size_t(j - 1) * size_t(p) + size_t(i - 1)) * size_t(NB) * NB;
+}
+template <int NB>
+__device__ __forceinline__ size_t soff(int p, int i, int k) {
+  return (size_t(k - 1) * size_t(p) + size_t(i - 1)) * size_t(IB) * NB;
+}
+
+template <int NB, bool TRANST>
+__global__ void __launch_bounds__(NT, 1) exec_kernel(ExecParams P) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_item;
+  const int tid = threadIdx.x;
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(P.queue, 1);
+    __syncthreads();
+    const int it = s_item;
+    if (it >= P.n_items) break;
+    const Item I = P.items[it];
+    if (tid < 32) {
+      for (int t = tid; t < I.pred_n; t += 32) {
+        const int pr = P.preds[I.pred_lo + t];
+        while (ld_acquire(P.done + pr) == 0) __nanosleep(40);
+      }
+      __syncwarp();
+      __threadfence();  // gpu-scope fence: also drops stale L1 lines
+    }
+    __syncthreads();
+    switch (I.kind) {
+      case tqr::GEQRT:
+        if constexpr (TRANST)
+          panel_item<NB, GE>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), nullptr, P.tg + soff<NB>(P.p, I.i, I.k), tid);
+        break;
+      case tqr::TTQRT:
+        if constexpr (TRANST)
+          panel_item<NB, TT>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.k),
+                             P.te + soff<NB>(P.p, I.i, I.k), tid);
+        break;
+      case tqr::TSQRT:
+        if constexpr (TRANST)
+          panel_item<NB, TS>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.k),
+                             P.te + soff<NB>(P.p, I.i, I.k), tid);
+        break;
+      case tqr::UNMQR:
+        update_item<NB, GE, TRANST>(sm, P.vtiles + toff<NB>(P.p, I.i, I.k), P.tg + soff<NB>(P.p, I.i, I.k),
+                                    P.tiles + toff<NB>(P.p, I.i, I.j), nullptr, I.slab, tid);
+        break;
+      case tqr::TTMQR:
+        update_item<NB, TT, TRANST>(sm, P.vtiles + toff<NB>(P.p, I.i, I.k), P.te + soff<NB>(P.p, I.i, I.k),
+                                    P.tiles + toff<NB>(P.p, I.i, I.j), P.tiles + toff<NB>(P.p, I.piv, I.j), I.slab,
+                                    tid);
+        break;
+      case tqr::TSMQR:
+        update_item<NB, TS, TRANST>(sm, P.vtiles + toff<NB>(P.p, I.i, I.k), P.te + soff<NB>(P.p, I.i, I.k),
+                                    P.tiles + toff<NB>(P.p, I.i, I.j), P.tiles + toff<NB>(P.p, I.piv, I.j), I.slab,
+                                    tid);
+        break;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(P.done + it, 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pack / unpack / R extraction (HBM-bound copies through a 32x33 smem tile)
+
+__global__ void pack_kernel(const double* __restrict__ A, int64_t lda, int row_major, double* __restrict__ tiles,
+                            int p, int q, int nb) {
+  __shared__ double t[32][33];
+  const int sub = nb / 32;
+  const int64_t blk = blockIdx.x;  // over tiles x sub x sub
+  const int64_t tile = blk / (sub * sub);
+  const int s = int(blk % (sub * sub));
+  const int ti = int(tile % p), tj = int(tile / p);
+  const int ra = (s % sub) * 32, cb = (s / sub) * 32;  // row/col offset inside the tile
+  const int64_t grow = int64_t(ti) * nb + ra, gcol = int64_t(tj) * nb + cb;
+  double* dst = tiles + size_t(tile) * nb * nb;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  if (row_major) {
+    for (int y = ty; y < 32; y += 8) t[y][tx] = A[(grow + y) * lda + gcol + tx];  // t[row][col]
+    __syncthreads();
+    for (int y = ty; y < 32; y += 8) dst[(ra + tx) + size_t(cb + y) * nb] = t[tx][y];
+  } else {
+    for (int y = ty; y < 32; y += 8) dst[(ra + tx) + size_t(cb + y) * nb] = A[(gcol + y) * lda + grow + tx];
+  }
+}
+
+__global__ void unpack_kernel(const double* __restrict__ tiles, int p, int q, int nb, double* __restrict__ A,
+                              int64_t lda, int row_major, int upper_only, int64_t col_off) {
+  __shared__ double t[32][33];
+  const int sub = nb / 32;
+  const int64_t blk = blockIdx.x;
+  const int64_t tile = blk / (sub * sub);
+  const int s = int(blk % (sub * sub));
+  const int ti = int(tile % p), tj = int(tile / p);
+  const int ra = (s % sub) * 32, cb = (s / sub) * 32;
+  const int64_t grow = int64_t(ti) * nb + ra, gcol = int64_t(tj) * nb + cb;
+  const double* src = tiles + size_t(tile) * nb * nb;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  auto val = [&](int r, int c) {
+    double v = src[r + size_t(c) * nb];
+    if (upper_only && int64_t(ti) * nb + r > col_off + int64_t(tj) * nb + c) v = 0.0;
+    return v;
+  };
+  if (row_major) {
+    for (int y = ty; y < 32; y += 8) t[y][tx] = val(ra + tx, cb + y);  // t[col][row]
+    __syncthreads();
+    for (int y = ty; y < 32; y += 8) A[(grow + y) * lda + gcol + tx] = t[tx][y];
+  } else {
+    for (int y = ty; y < 32; y += 8) A[(gcol + y) * lda + grow + tx] = val(ra + tx, cb + y);
+  }
+}
+
+// FP64 peak probe: 8 independent DMMA chains per warp, 8 warps x 2 CTAs per SM
+__global__ void __launch_bounds__(256) peak_kernel(double* out, int iters) {
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  const double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma(c[i], a, b);
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 1234.5) out[0] = s;
+}
+
+// ---------------------------------------------------------------------------
+// host: schedule compilation
+
+struct DevSched {
+  Item* items = nullptr;
+  int32_t* preds = nullptr;
+  int* done = nullptr;
+  int* queue = nullptr;
+  int n_items = 0;
+  int64_t n_preds = 0;
+  void free_all() {
+    cudaFree(items);
+    cudaFree(preds);
+    cudaFree(done);
+    cudaFree(queue);
+    items = nullptr;
+    preds = nullptr;
+    done = nullptr;
+    queue = nullptr;
+  }
+};
+
+struct Task {
+  int8_t kind;
+  int32_t i, piv, k, j;
+};
+
+inline bool is_update(int kind) { return kind == tqr::UNMQR || kind == tqr::TTMQR || kind == tqr::TSMQR; }
+
+// tasks in execution order + incoming task edges -> slab items + pred CSR
+void expand(const std::vector<Task>& tasks, const std::vector<std::vector<int32_t>>& in_edges,
+            const std::vector<int32_t>& order, int slabs, std::vector<Item>& items, std::vector<int32_t>& preds) {
+  const size_t n = tasks.size();
+  std::vector<int32_t> first(n), nitems(n);
+  int32_t pos = 0;
+  for (int32_t t : order) {
+    first[size_t(t)] = pos;
+    nitems[size_t(t)] = is_update(tasks[size_t(t)].kind) ? slabs : 1;
+    pos += nitems[size_t(t)];
+  }
+  items.clear();
+  items.reserve(size_t(pos));
+  preds.clear();
+  std::vector<int32_t> tmp;
+  for (int32_t t : order) {
+    const Task& T = tasks[size_t(t)];
+    for (int s = 0; s < nitems[size_t(t)]; ++s) {
+      tmp.clear();
+      for (int32_t u : in_edges[size_t(t)]) {
+        if (is_update(tasks[size_t(u)].kind) && is_update(T.kind)) {
+          tmp.push_back(first[size_t(u)] + s);
+        } else {
+          for (int x = 0; x < nitems[size_t(u)]; ++x) tmp.push_back(first[size_t(u)] + x);
+        }
+      }
+      std::sort(tmp.begin(), tmp.end());
+      tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+      Item it{};
+      it.kind = T.kind;
+      it.slab = int8_t(s);
+      it.i = T.i;
+      it.piv = T.piv;
+      it.k = T.k;
+      it.j = T.j;
+      it.pred_lo = int32_t(preds.size());
+      it.pred_n = int32_t(tmp.size());
+      preds.insert(preds.end(), tmp.begin(), tmp.end());
+      items.push_back(it);
+    }
+  }
+}
+
+void upload(DevSched& d, const std::vector<Item>& items, const std::vector<int32_t>& preds) {
+  d.n_items = int(items.size());
+  d.n_preds = int64_t(preds.size());
+  auto ck = [](cudaError_t e) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+  };
+  ck(cudaMalloc(&d.items, std::max<size_t>(1, items.size()) * sizeof(Item)));
+  ck(cudaMalloc(&d.preds, std::max<size_t>(1, preds.size()) * sizeof(int32_t)));
+  ck(cudaMalloc(&d.done, std::max<size_t>(1, items.size()) * sizeof(int)));
+  ck(cudaMalloc(&d.queue, sizeof(int)));
+  ck(cudaMemcpy(d.items, items.data(), items.size() * sizeof(Item), cudaMemcpyHostToDevice));
+  if (!preds.empty()) ck(cudaMemcpy(d.preds, preds.data(), preds.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+}
+
+}  // namespace
+
+struct tqr_plan {
+  int p = 0, q = 0, nb = 0, ib = IB, ts = 0;
+  int64_t n_tasks = 0;
+  double flops = 0;
+  std::vector<Task> trace;  // factorization trace (for apply-Q)
+  DevSched fac;
+  std::map<std::pair<int, int>, DevSched> aq;  // (trans, c_cols) -> apply-Q schedule
+  ~tqr_plan() {
+    fac.free_all();
+    for (auto& kv : aq) kv.second.free_all();
+  }
+};
+
+namespace {
+
+int num_sms() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+template <int NB, bool TRANST>
+cudaError_t launch_exec(const DevSched& d, const double* vtiles, double* tiles, double* tg, double* te, int p,
+                        cudaStream_t st) {
+  auto kern = exec_kernel<NB, TRANST>;
+  const size_t smem = Smem<NB>::BYTES;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(d.done, 0, size_t(std::max(d.n_items, 1)) * sizeof(int), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(d.queue, 0, sizeof(int), st)) != cudaSuccess) return e;
+  if (d.n_items == 0) return cudaSuccess;
+  ExecParams P{d.items, d.preds, d.n_items, d.done, d.queue, vtiles, tiles, tg, te, p};
+  const int grid = std::min(d.n_items, num_sms());
+  kern<<<grid, NT, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t run(const DevSched& d, int nb, bool transT, const double* vtiles, double* tiles, double* tg, double* te,
+                int p, cudaStream_t st) {
+  switch (nb) {
+    case 64:
+      return transT ? launch_exec<64, true>(d, vtiles, tiles, tg, te, p, st)
+                    : launch_exec<64, false>(d, vtiles, tiles, tg, te, p, st);
+    case 128:
+      return transT ? launch_exec<128, true>(d, vtiles, tiles, tg, te, p, st)
+                    : launch_exec<128, false>(d, vtiles, tiles, tg, te, p, st);
+    case 256:
+      return transT ? launch_exec<256, true>(d, vtiles, tiles, tg, te, p, st)
+                    : launch_exec<256, false>(d, vtiles, tiles, tg, te, p, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+
+int cuda_guarded(cudaError_t e) {
+  if (e == cudaSuccess) return TQR_OK;
+  tqr::g_err = std::string("CUDA: ") + cudaGetErrorString(e);
+  return TQR_ECUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tqr_plan_create(const tqr_build* hb, int nb, int ib, tqr_plan** out) {
+  return tqr::guard([&] {
+    if (!hb || !hb->b) throw tqr::ValueError("null build");
+    const tqr::Build& b = *hb->b;
+    if (!b.keep_trace) throw tqr::ValueError("plan needs a build made with keep_trace=True");
+    if (nb != 64 && nb != 128 && nb != 256) throw tqr::ValueError("nb must be 64, 128 or 256");
+    if (ib != IB) throw tqr::ValueError("ib must be 32");
+    auto* P = new tqr_plan;
+    try {
+      P->p = b.p;
+      P->q = b.q;
+      P->nb = nb;
+      P->ib = ib;
+      P->ts = b.ts;
+      const size_t n = b.trace.size();
+      P->n_tasks = int64_t(n);
+      P->trace.resize(n);
+      for (size_t t = 0; t < n; ++t) {
+        const auto& R = b.trace[t];
+        Task T{R.kind, R.a, -1, -1, -1};
+        switch (R.kind) {
+          case tqr::GEQRT: T.k = R.b; break;
+          case tqr::UNMQR: T.k = R.b; T.j = R.c; break;
+          case tqr::TTQRT:
+          case tqr::TSQRT: T.piv = R.b; T.k = R.c; break;
+          default: T.piv = R.b; T.k = R.c; T.j = R.d; break;
+        }
+        P->trace[t] = T;
+      }
+      // hazard edges of the reference model, weighted ASAP order (QR weights)
+      auto edges = tqr::hazard_edges(b);
+      std::vector<std::vector<int32_t>> in(n);
+      for (const auto& e : edges) in[size_t(e.v)].push_back(e.u);
+      static const int64_t W[6] = {4, 2, 6, 6, 6, 12};
+      std::vector<int64_t> est(n, 0);
+      for (size_t v = 0; v < n; ++v)
+        for (int32_t u : in[v]) est[v] = std::max(est[v], est[size_t(u)] + W[P->trace[size_t(u)].kind]);
+      std::vector<int32_t> order(n);
+      std::iota(order.begin(), order.end(), 0);
+      std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t c) { return est[size_t(a)] < est[size_t(c)]; });
+      std::vector<Item> items;
+      std::vector<int32_t> preds;
+      expand(P->trace, in, order, nb / WS, items, preds);
+      upload(P->fac, items, preds);
+      const double m = double(b.p) * nb, nn = double(b.q) * nb;
+      P->flops = 2.0 * nn * nn * (m - nn / 3.0);
+    } catch (...) {
+      delete P;
+      throw;
+    }
+    *out = P;
+  });
+}
+
+int tqr_plan_get_info(const tqr_plan* P, tqr_plan_info* o) {
+  return tqr::guard([&] {
+    o->p = P->p;
+    o->q = P->q;
+    o->nb = P->nb;
+    o->ib = P->ib;
+    o->slab = WS;
+    o->family_ts = P->ts;
+    o->n_tasks = P->n_tasks;
+    o->n_items = P->fac.n_items;
+    o->n_preds = P->fac.n_preds;
+    o->tg_stride = int64_t(P->ib) * P->nb;
+    o->te_stride = int64_t(P->ib) * P->nb;
+    o->flops_alg = P->flops;
+  });
+}
+
+void tqr_plan_free(tqr_plan* P) { delete P; }
+
+int tqr_factor(tqr_plan* P, double* tiles, double* tg, double* te, void* stream) {
+  int rc = tqr::guard([&] {
+    if (!P) throw tqr::ValueError("null plan");
+  });
+  if (rc) return rc;
+  return cuda_guarded(run(P->fac, P->nb, true, tiles, tiles, tg, te, P->p, static_cast<cudaStream_t>(stream)));
+}
+
+int tqr_apply_q(tqr_plan* P, int trans, const double* tiles, const double* tg, const double* te, double* c_tiles,
+                int c_cols, void* stream) {
+  int rc = tqr::guard([&] {
+    if (!P) throw tqr::ValueError("null plan");
+    if (c_cols < 1) throw tqr::ValueError("c_cols must be >= 1");
+    auto key = std::make_pair(trans ? 1 : 0, c_cols);
+    if (P->aq.count(key)) return;
+    // reflector replay: forward trace order for Q^T, reverse for Q
+    // (oracle recipe: SURVEY.md App. B.1 step 4); updates skipped.
+    std::vector<Task> tasks;
+    const size_t n = P->trace.size();
+    for (size_t s = 0; s < n; ++s) {
+      const Task& T = P->trace[trans ? s : n - 1 - s];
+      int8_t kind;
+      if (T.kind == tqr::GEQRT)
+        kind = tqr::UNMQR;
+      else if (T.kind == tqr::TTQRT)
+        kind = tqr::TTMQR;
+      else if (T.kind == tqr::TSQRT)
+        kind = tqr::TSMQR;
+      else
+        continue;
+      for (int j = 1; j <= c_cols; ++j) tasks.push_back({kind, T.i, T.piv, T.k, j});
+    }
+    // hazards: each task reads-modifies-writes C(i,j) (and C(piv,j))
+    const size_t m = tasks.size();
+    std::vector<std::vector<int32_t>> in(m);
+    std::vector<int32_t> last(size_t(P->p + 1) * size_t(c_cols + 1), -1);
+    std::vector<int64_t> est(m, 0);
+    static const int64_t W[6] = {4, 2, 6, 6, 6, 12};
+    for (size_t t = 0; t < m; ++t) {
+      const Task& T = tasks[t];
+      int rows[2] = {T.i, T.piv};
+      for (int x = 0; x < (T.kind == tqr::UNMQR ? 1 : 2); ++x) {
+        int32_t& L = last[size_t(rows[x]) * size_t(c_cols + 1) + size_t(T.j)];
+        if (L >= 0) {
+          in[t].push_back(L);
+          est[t] = std::max(est[t], est[size_t(L)] + W[tasks[size_t(L)].kind]);
+        }
+        L = int32_t(t);
+      }
+    }
+    std::vector<int32_t> order(m);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t c) { return est[size_t(a)] < est[size_t(c)]; });
+    std::vector<Item> items;
+    std::vector<int32_t> preds;
+    expand(tasks, in, order, P->nb / WS, items, preds);
+    DevSched d;
+    upload(d, items, preds);
+    P->aq[key] = d;
+  });
+  if (rc) return rc;
+  const DevSched& d = P->aq[std::make_pair(trans ? 1 : 0, c_cols)];
+  return cuda_guarded(run(d, P->nb, trans != 0, tiles, c_tiles, const_cast<double*>(tg), const_cast<double*>(te),
+                          P->p, static_cast<cudaStream_t>(stream)));
+}
+
+int tqr_pack(const double* A, int64_t lda, int row_major, double* tiles, int p, int q, int nb, void* stream) {
+  int rc = tqr::guard([&] {
+    if (nb % 32) throw tqr::ValueError("nb must be a multiple of 32");
+  });
+  if (rc) return rc;
+  const int64_t blocks = int64_t(p) * q * (nb / 32) * (nb / 32);
+  pack_kernel<<<unsigned(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(A, lda, row_major, tiles, p, q, nb);
+  return cuda_guarded(cudaGetLastError());
+}
+
+int tqr_unpack(const double* tiles, int p, int q, int nb, double* A, int64_t lda, int row_major, void* stream) {
+  const int64_t blocks = int64_t(p) * q * (nb / 32) * (nb / 32);
+  unpack_kernel<<<unsigned(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(tiles, p, q, nb, A, lda, row_major,
+                                                                                0, 0);
+  return cuda_guarded(cudaGetLastError());
+}
+
+int tqr_extract_r(const double* tiles, int p, int q, int nb, double* R, int64_t ldr, int row_major, void* stream) {
+  // R = upper triangle of tile rows 1..q; the first q tiles of each tile
+  // column are contiguous, so each tile column is a q x 1 tile grid.
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t blocks_j = int64_t(q) * (nb / 32) * (nb / 32);
+  for (int j = 0; j < q; ++j) {
+    const double* col = tiles + size_t(j) * size_t(p) * size_t(nb) * nb;
+    double* dst = row_major ? R + size_t(j) * nb : R + size_t(j) * nb * size_t(ldr);
+    unpack_kernel<<<unsigned(blocks_j), 256, 0, st>>>(col, q, 1, nb, dst, ldr, row_major, 1, int64_t(j) * nb);
+  }
+  return cuda_guarded(cudaGetLastError());
+}
+
+int tqr_fp64_peak(double* tflops_out, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(double));
+  if (e != cudaSuccess) return cuda_guarded(e);
+  const int sms = num_sms();
+  const int iters = 20000, blocks = 2 * sms;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  peak_kernel<<<blocks, 256, 0, st>>>(d, 1000);
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    cudaEventRecord(e0, st);
+    peak_kernel<<<blocks, 256, 0, st>>>(d, iters);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = std::min(best, ms);
+  }
+  e = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_guarded(e);
+  const double flops = 2.0 * 256.0 * 8.0 * double(iters) * blocks * 8.0;
+  *tflops_out = flops / (double(best) * 1e-3) / 1e12;
+  return TQR_OK;
+}
+
+}  // extern "C"

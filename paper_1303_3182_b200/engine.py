@@ -1,0 +1,157 @@
+"""Numeric tiled QR on B200 (no reference counterpart: the reference runs no
+kernels, pkg/README.md:11-12).
+
+``tiled_qr(A, nb, algo=...)`` factors an m x n fp64 matrix with the tiled
+TT/TS kernels in the order fixed by the reference elimination tree
+(build_tree, qr.py:622-649; or any user list via tiled_build,
+qr.py:535-540).  Device memory and streams come from PyTorch; every kernel
+is in libtqr.so (csrc/).  There is no CPU fallback: without CUDA or without
+the library this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .qr import EliminationList, QrBuild, build_tree, tiled_build
+
+
+def _stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _vp(t):
+    return C.c_void_p(t.data_ptr())
+
+
+class Plan:
+    """A QrBuild compiled into a static device schedule for tile size nb
+    (tqr_plan_create).  Reusable across matrices of the same shape."""
+
+    def __init__(self, build: QrBuild, nb=256, ib=32):
+        if not torch.cuda.is_available():
+            raise RuntimeError("tiled QR needs a CUDA device (no CPU fallback)")
+        if build._h is None or not build.keep_trace:
+            raise ValueError("the plan needs a QrBuild made with keep_trace=True")
+        self.build = build
+        h = C.c_void_p()
+        check(lib().tqr_plan_create(build._h, int(nb), int(ib), C.byref(h)))
+        self._h = h
+        info = _lib.PlanInfo()
+        check(lib().tqr_plan_get_info(h, C.byref(info)))
+        self.info = info
+        self.p, self.q, self.nb, self.ib = info.p, info.q, info.nb, info.ib
+        self.m, self.n = self.p * self.nb, self.q * self.nb
+        self.flops = float(info.flops_alg)
+
+    def __del__(self):
+        h = self.__dict__.get("_h")
+        if h is not None and _lib._lib is not None:
+            _lib._lib.tqr_plan_free(h)
+
+    def alloc(self, device=None):
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        tiles = torch.empty(self.p * self.q * self.nb * self.nb, dtype=torch.float64, device=dev)
+        tg = torch.zeros(self.p * self.q * self.info.tg_stride, dtype=torch.float64, device=dev)
+        te = torch.zeros(self.p * self.q * self.info.te_stride, dtype=torch.float64, device=dev)
+        return tiles, tg, te
+
+    def pack(self, A, tiles, stream=None):
+        """Row-major (C-contiguous) or column-major m x n device matrix -> tiles."""
+        assert A.dtype == torch.float64 and A.is_cuda and A.shape == (self.m, self.n)
+        if A.is_contiguous():
+            check(lib().tqr_pack(_vp(A), A.stride(0), 1, _vp(tiles), self.p, self.q, self.nb, _stream_ptr(stream)))
+        elif A.t().is_contiguous():
+            check(lib().tqr_pack(_vp(A), A.stride(1), 0, _vp(tiles), self.p, self.q, self.nb, _stream_ptr(stream)))
+        else:
+            raise ValueError("A must be row- or column-major contiguous")
+
+    def factor(self, tiles, tg, te, stream=None):
+        check(lib().tqr_factor(self._h, _vp(tiles), _vp(tg), _vp(te), _stream_ptr(stream)))
+
+    def apply_q(self, trans, tiles, tg, te, c_tiles, c_cols, stream=None):
+        check(lib().tqr_apply_q(self._h, int(bool(trans)), _vp(tiles), _vp(tg), _vp(te), _vp(c_tiles),
+                                int(c_cols), _stream_ptr(stream)))
+
+    def extract_r(self, tiles, stream=None):
+        R = torch.empty((self.n, self.n), dtype=torch.float64, device=tiles.device)
+        check(lib().tqr_extract_r(_vp(tiles), self.p, self.q, self.nb, _vp(R), self.n, 1, _stream_ptr(stream)))
+        return R
+
+    def unpack(self, tiles, cols=None, stream=None):
+        cols = self.q if cols is None else cols
+        A = torch.empty((self.m, cols * self.nb), dtype=torch.float64, device=tiles.device)
+        check(lib().tqr_unpack(_vp(tiles), self.p, cols, self.nb, _vp(A), A.stride(0), 1, _stream_ptr(stream)))
+        return A
+
+    def pack_cols(self, A, cols, stream=None):
+        tiles = torch.empty(self.p * cols * self.nb * self.nb, dtype=torch.float64, device=A.device)
+        A = A.contiguous()
+        check(lib().tqr_pack(_vp(A), A.stride(0), 1, _vp(tiles), self.p, cols, self.nb, _stream_ptr(stream)))
+        return tiles
+
+
+class TiledQR:
+    """Result of a tiled QR: factored tiles (R + reflectors) and T factors."""
+
+    def __init__(self, plan: Plan, tiles, tg, te):
+        self.plan, self.tiles, self.tg, self.te = plan, tiles, tg, te
+
+    @property
+    def build(self):
+        return self.plan.build
+
+    def R(self):
+        return self.plan.extract_r(self.tiles)
+
+    def apply_q(self, C_mat, trans=False):
+        """Q @ C (trans=False) or Q^T @ C (trans=True) for an m x c device matrix."""
+        P = self.plan
+        cols = C_mat.shape[1] // P.nb
+        assert C_mat.shape == (P.m, cols * P.nb)
+        ct = P.pack_cols(C_mat, cols)
+        P.apply_q(trans, self.tiles, self.tg, self.te, ct, cols)
+        return P.unpack(ct, cols)
+
+    def Q(self):
+        """Explicit m x n Q (reverse reflector replay on [I; 0])."""
+        P = self.plan
+        E = torch.zeros((P.m, P.n), dtype=torch.float64, device=self.tiles.device)
+        E[:P.n].fill_diagonal_(1.0)
+        return self.apply_q(E, trans=False)
+
+
+def tiled_qr(A, nb=256, ib=32, algo="greedy", family="TT", bs=None, grasap_i=1, elim=None, plan=None):
+    """Tiled QR of an m x n fp64 matrix (m = p nb, n = q nb, p >= q).
+
+    The elimination tree is ``build_tree(p, q, algo, family, bs, grasap_i)``
+    or the given EliminationList ``elim`` (validated, tiled_build).  A on the
+    host is copied to the current device.  Returns a TiledQR.
+    """
+    if not torch.cuda.is_available():
+        raise RuntimeError("tiled QR needs a CUDA device (no CPU fallback)")
+    A = torch.as_tensor(A, dtype=torch.float64)
+    m, n = A.shape
+    if m % nb or n % nb:
+        raise ValueError(f"matrix {m}x{n} is not a whole number of {nb}x{nb} tiles")
+    p, q = m // nb, n // nb
+    if plan is None:
+        if elim is not None:
+            if not isinstance(elim, EliminationList):
+                raise TypeError("elim must be an EliminationList")
+            if (elim.p, elim.q) != (p, q):
+                raise ValueError(f"list is for {elim.p}x{elim.q} tiles, matrix has {p}x{q}")
+            build = tiled_build(elim, family)
+        else:
+            build = build_tree(p, q, algo, family=family, bs=bs, grasap_i=grasap_i)
+        plan = Plan(build, nb, ib)
+    if not A.is_cuda:
+        A = A.cuda()
+    tiles, tg, te = plan.alloc(A.device)
+    plan.pack(A, tiles)
+    plan.factor(tiles, tg, te)
+    return TiledQR(plan, tiles, tg, te)

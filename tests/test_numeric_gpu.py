@@ -1,0 +1,131 @@
+"""GPU parity of the tiled QR kernels (through the C ABI) against the LAPACK
+replay oracle of the reference trace (oracle/replay.py).
+
+Tolerances (fp64): tile contents (R, V, T) elementwise within 1e-11 * scale;
+R after row-sign normalisation within 1e-11 * ||A||_F (north_star);
+||A - QR||_F / ||A||_F and ||Q^T Q - I||_F within 1e-12 (north_star).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1303_3182_b200 as P  # noqa: E402
+from paper_1303_3182_b200.engine import Plan, TiledQR, tiled_qr  # noqa: E402
+from oracle.replay import Replay, replay_build, row_sign_normalize  # noqa: E402
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _run(build, A, nb):
+    plan = Plan(build, nb)
+    At = torch.from_numpy(A).cuda()
+    tiles, tg, te = plan.alloc()
+    plan.pack(At, tiles)
+    plan.factor(tiles, tg, te)
+    torch.cuda.synchronize()
+    return plan, TiledQR(plan, tiles, tg, te)
+
+
+def _compare_tiles(res, rp, scale, what):
+    t = res.tiles.cpu().numpy()
+    ref = rp.tiles_array()
+    err = np.abs(t - ref).max()
+    assert err <= 1e-11 * scale, (what, "tiles", err)
+    for which, arr in (("G", res.tg), ("E", res.te)):
+        d = np.abs(arr.cpu().numpy() - rp.t_array(which)).max()
+        assert d <= 1e-11 * max(scale, 1.0), (what, "T" + which, d)
+
+
+CASES = [
+    # (p, q, nb, algo, family, bs)
+    (1, 1, 64, "greedy", "TT", None),
+    (2, 1, 64, "greedy", "TT", None),
+    (2, 2, 64, "flattree", "TT", None),
+    (3, 2, 64, "flattree", "TS", None),
+    (8, 4, 64, "greedy", "TT", None),          # C1 shape
+    (8, 4, 64, "fibonacci", "TT", None),
+    (8, 4, 64, "plasmatree", "TT", 4),
+    (8, 4, 64, "flattree", "TS", None),
+    (8, 4, 64, "grasap", "TT", None),
+    (6, 3, 64, "greedy", "TS", None),          # mixed TS/TT kernels
+    (3, 2, 128, "greedy", "TT", None),
+    (4, 2, 256, "greedy", "TT", None),
+    (3, 2, 256, "flattree", "TS", None),
+]
+
+
+@pytest.mark.parametrize("p,q,nb,algo,family,bs", CASES)
+def test_tiles_match_lapack_replay(p, q, nb, algo, family, bs):
+    _need_gpu()
+    rng = np.random.default_rng(100 + p * 7 + q)
+    A = rng.standard_normal((p * nb, q * nb))
+    b = P.build_tree(p, q, algo, family=family, bs=bs)
+    plan, res = _run(b, A, nb)
+    rp = replay_build(A, b, nb)
+    scale = np.linalg.norm(A)
+    _compare_tiles(res, rp, scale, (p, q, nb, algo, family))
+    R = res.R().cpu().numpy()
+    assert np.linalg.norm(R - rp.r()) <= 1e-11 * scale
+
+
+def test_c1_greedy_full_checks():
+    """BASELINE config 1: 512x256, nb=64, Greedy/TT, N(0,1) seed 0."""
+    _need_gpu()
+    A = np.random.default_rng(0).standard_normal((512, 256))
+    res = tiled_qr(A, nb=64, algo="greedy")
+    b = res.build
+    assert b.cp == 78 and len(b.elim) == 22
+    R = res.R().cpu().numpy()
+    Rref = np.linalg.qr(A, mode="r")
+    nA = np.linalg.norm(A)
+    assert np.linalg.norm(row_sign_normalize(R) - row_sign_normalize(Rref)) <= 1e-11 * nA
+    Q = res.Q()
+    At = torch.from_numpy(A).cuda()
+    Rt = torch.from_numpy(R).cuda()
+    assert (torch.linalg.norm(At - Q @ Rt) / nA).item() <= 1e-12
+    eye = torch.eye(256, dtype=torch.float64, device="cuda")
+    assert torch.linalg.norm(Q.T @ Q - eye).item() <= 1e-12
+
+
+@pytest.mark.parametrize("algo,family,bs", [("flattree", "TS", None), ("fibonacci", "TT", None),
+                                            ("greedy", "TT", None), ("plasmatree", "TT", 4),
+                                            ("grasap", "TT", None)])
+def test_c2_trees_agree(algo, family, bs):
+    """BASELINE config 2: same matrix (seed 1) per tree; R agrees up to row signs."""
+    _need_gpu()
+    A = np.random.default_rng(1).standard_normal((512, 256))
+    Rref = row_sign_normalize(np.linalg.qr(A, mode="r"))
+    res = tiled_qr(A, nb=64, algo=algo, family=family, bs=bs)
+    R = row_sign_normalize(res.R().cpu().numpy())
+    assert np.linalg.norm(R - Rref) <= 1e-11 * np.linalg.norm(A)
+
+
+def test_apply_qt_recovers_r():
+    _need_gpu()
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((6 * 128, 3 * 128))
+    res = tiled_qr(A, nb=128, algo="greedy")
+    At = torch.from_numpy(A).cuda()
+    QtA = res.apply_q(At, trans=True)
+    R = res.R()
+    n = 3 * 128
+    assert torch.linalg.norm(QtA[:n] - R).item() <= 1e-12 * np.linalg.norm(A)
+    assert torch.linalg.norm(QtA[n:]).item() <= 1e-12 * np.linalg.norm(A)
+
+
+def test_user_list_with_reverse_entries():
+    _need_gpu()
+    rng = np.random.default_rng(9)
+    E = P.ElimEntry
+    # 4x2 tiles; column 1 has a reverse elimination (i < piv)
+    lst = P.EliminationList(4, 2, [E(3, 4, 1), E(4, 1, 1), E(2, 1, 1), E(3, 2, 2), E(4, 2, 2)])
+    lst.validate()
+    A = rng.standard_normal((4 * 64, 2 * 64))
+    res = tiled_qr(A, nb=64, elim=lst)
+    rp = replay_build(A, res.build, 64)
+    _compare_tiles(res, rp, np.linalg.norm(A), "reverse")

@@ -117,6 +117,13 @@ int tqr_factor(tqr_plan* plan, double* tiles, double* tg, double* te, void* stre
  * replaying the trace's reflectors (forward for Q^T, reverse for Q).      */
 int tqr_apply_q(tqr_plan* plan, int trans, const double* tiles, const double* tg, const double* te,
                 double* c_tiles, int c_cols, void* stream);
+/* Diagnostics: record {t_dequeue, t_ready, t_end, smid} (globaltimer ns) per
+ * work item of the following tqr_factor/tqr_apply_q calls into trace_dev
+ * (4*n_items uint64; NULL disables); tqr_plan_items lists the items
+ * (kind, slab, i, piv, k, j, n_preds) in device order.  Gantt export as in
+ * the reference's list-schedule CSV (sched.py:36-49).                     */
+int tqr_set_trace(void* trace_dev);
+int tqr_plan_items(const tqr_plan* plan, int32_t* out7);
 /* Device-side FP64 peak probe (DMMA.8x8x4 loop on every SM), TFLOP/s.      */
 int tqr_fp64_peak(double* tflops_out, void* stream);
 

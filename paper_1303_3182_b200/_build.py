@@ -9,6 +9,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -39,7 +40,7 @@ def _run(cmd):
 
 def build(verbose=False):
     os.makedirs(BUILD, exist_ok=True)
-    objs = []
+    objs, jobs = [], []
     for src in sorted(os.listdir(CSRC)):
         if not src.endswith((".cpp", ".cu")):
             continue
@@ -54,7 +55,11 @@ def build(verbose=False):
                 cmd += ["-x", "c++"]
             if verbose:
                 print(" ".join(cmd))
-            _run(cmd)
+            jobs.append(cmd)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for r in ex.map(_run, jobs):
+            if verbose:
+                sys.stdout.write(r.stdout + r.stderr)
     if not os.path.exists(OUT) or any(os.path.getmtime(o) > os.path.getmtime(OUT) for o in objs):
         _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", OUT] + objs + ["-lpthread", "-ldl", "-lrt"])
     return OUT

@@ -69,6 +69,8 @@ SIGNATURES = {
     "tqr_factor": (C.c_int, [vp, vp, vp, vp, vp]),
     "tqr_apply_q": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, C.c_int, vp]),
     "tqr_fp64_peak": (C.c_int, [f64p, vp]),
+    "tqr_set_trace": (C.c_int, [vp]),
+    "tqr_plan_items": (C.c_int, [vp, i32p]),
 }
 
 _lib = None

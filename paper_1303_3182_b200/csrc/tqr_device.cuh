@@ -22,8 +22,44 @@
 
 namespace tqrk {
 
-constexpr int NT = 256;  // threads per CTA (8 warps)
+#ifdef TQR_PROF_UPD
+__device__ unsigned long long g_uprof[16];
+#define UPROF_MARK(k) UPROF_MARK_V(k, _tp)
+#define UPROF_MARK_V(k, v)                                                    \
+  do {                                                                        \
+    if ((threadIdx.x & 31) == 0) {                                            \
+      long long _t = clock64();                                               \
+      atomicAdd(&g_uprof[k], (unsigned long long)(_t - v));                   \
+      v = _t;                                                                 \
+    }                                                                         \
+  } while (0)
+#define UPROF_DECL long long _tp = clock64()
+#define UPROF_DECL_V(v) long long v = clock64()
+#else
+#define UPROF_MARK(k) \
+  do {                \
+  } while (0)
+#define UPROF_MARK_V(k, v) \
+  do {                     \
+  } while (0)
+#define UPROF_DECL
+#define UPROF_DECL_V(v)
+#endif
+
+constexpr int NT = 256;  // compute threads per CTA (8 warps)
 constexpr int NW = 8;
+constexpr int NTP = NT + 128;  // + one producer warpgroup (staging / prefetch)
+
+// all threads of the CTA (both warp roles)
+__device__ __forceinline__ void bar_all() { asm volatile("bar.sync 0, 384;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N));
+}
 constexpr int IB = 32;   // inner blocking ib
 constexpr int WS = 64;   // columns per update work item (8 per warp)
 
@@ -33,8 +69,9 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// in-sub-block swizzle: element (a, b) of an 8x8 sub-block -> 0..63 such that
-// for lane (r,c): {(2c+h, r)} and {(r, 2c+h)} each hit 16 distinct 8-byte
+// in-sub-block swizzle: element (a, b) (row, col) of an 8x8 sub-block ->
+// 0..63 such that the DMMA B-fragment reads of lane (r, c), {(2c+h, r)}
+// (W = V^T X) and {(r, 2c+h)} (X -= W V^T), each hit 16 distinct 8-byte
 // banks per half-warp.
 __device__ __forceinline__ int swz_in(int a, int b) {
   const int a0 = a & 1, a1 = (a >> 1) & 1, a2 = (a >> 2) & 1;
@@ -53,6 +90,11 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
+// bulk L2 prefetch of a contiguous range (bytes, multiple of 16)
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -71,13 +113,31 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 enum Mode : int { GE = 0, TT = 1, TS = 2 };
 
 // Apply one ib-block reflector H_b = I - V T V^T (or its transpose) to the
-// warp's 8 columns held in x (rows of groups [g0, g1)), plus the IB "top"
-// rows at `top` (TT/TS: the pivot tile's block rows; nullptr for GE).
+// warp's 8 columns held in x, rows of the IB-row blocks [rb0, rb1), plus the
+// IB "top" rows at `top` (TT/TS: the pivot tile's block rows; nullptr for
+// GE).
 //   Q^T: W = top + V^T X ; W = T^T W ; top -= W ; X -= V W   (TRANST = true)
 //   Q  : same with W = T W                                  (TRANST = false)
-template <int NB, bool TRANST>
-__device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int g0, int g1, const double* __restrict__ Vs,
-                                           const double* __restrict__ Ts, double* top, int lane) {
+// The row loop is unrolled per 32-row block (4 DMMA row groups) so the
+// B-fragment loads of a block are scheduled ahead of its DMMAs.
+struct NoPf {
+  __device__ __forceinline__ void operator()() const {}
+  __device__ __forceinline__ void flush() const {}
+};
+
+// MASK (GE unit-lower / TT upper-triangular / TS none) is applied to the
+// B fragments of row block `drb` (the reflector block's diagonal 32x32).
+template <int NB, bool TRANST, int MASK, class PF = NoPf>
+__device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int rb1, const double* __restrict__ Vs,
+                                           const double* __restrict__ Ts, double* top, int lane,
+                                           const double* top_s = nullptr, int drb = -1, PF pf = PF()) {
+  // diagonal-block mask of V(row, col), block-local coordinates
+  auto vmask = [](double v, int row, int col) {
+    if (MASK == 0) return (row > col) ? v : (row == col ? 1.0 : 0.0);  // GE
+    if (MASK == 1) return (row <= col) ? v : 0.0;                        // TT
+    return v;
+  };
+  UPROF_DECL_V(_tq);
   const int r = lane >> 2, c = lane & 3;
   const int s1a = swz_in(2 * c, r), s1b = swz_in(2 * c + 1, r);  // (2c+h, r)
   const int s3a = swz_in(r, 2 * c), s3b = swz_in(r, 2 * c + 1);  // (r, 2c+h)
@@ -85,42 +145,90 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int g0, int g
   if (top) {
 #pragma unroll
     for (int nb = 0; nb < 4; ++nb) {
-      double2 v = ldcg2(top + 8 * nb + 2 * c + r * NB);
+      // top_s: the block's IB top rows of this warp's 8 columns staged in
+      // smem (column-major, ld IB); else read from global
+      double2 v = top_s ? *reinterpret_cast<const double2*>(top_s + 8 * nb + 2 * c + r * IB)
+                        : ldcg2(top + 8 * nb + 2 * c + r * NB);
       ap[nb][0] = v.x;
       ap[nb][1] = v.y;
-      w[nb][0] = v.x;
-      w[nb][1] = v.y;
     }
   } else {
 #pragma unroll
-    for (int nb = 0; nb < 4; ++nb) w[nb][0] = w[nb][1] = ap[nb][0] = ap[nb][1] = 0.0;
+    for (int nb = 0; nb < 4; ++nb) ap[nb][0] = ap[nb][1] = 0.0;
   }
-  // W^T (8 x IB) += X (8 x rows) * V (rows x IB)
 #pragma unroll
-  for (int g = 0; g < NB / 8; ++g) {
-    if (g >= g0 && g < g1) {
-      const double* vb = Vs + g * (IB / 8) * 64;
+  for (int nb = 0; nb < 4; ++nb) {
+    w[nb][0] = ap[nb][0];
+    w[nb][1] = ap[nb][1];
+  }
+  // W^T (8 x IB) += X (8 x rows) * V (rows x IB); B fragments of the next
+  // row group are loaded while the current group's DMMAs issue
+#pragma unroll
+  for (int rb = 0; rb < NB / IB; ++rb) {
+    if (rb >= rb0 && rb < rb1) {
+      const bool dg = (MASK != 2) && rb == drb;
+      double bc[2][4], bn[2][4];
 #pragma unroll
       for (int nb = 0; nb < 4; ++nb) {
-        dmma(w[nb], x[g][0], vb[nb * 64 + s1a]);
-        dmma(w[nb], x[g][1], vb[nb * 64 + s1b]);
+        const double* vb = Vs + ((rb * 4) * (IB / 8) + nb) * 64;
+        bc[0][nb] = vb[s1a];
+        bc[1][nb] = vb[s1b];
+        if (dg) {
+          bc[0][nb] = vmask(bc[0][nb], 2 * c, 8 * nb + r);
+          bc[1][nb] = vmask(bc[1][nb], 2 * c + 1, 8 * nb + r);
+        }
+      }
+#pragma unroll
+      for (int gg = 0; gg < 4; ++gg) {
+        if (gg < 3) {
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) {
+            const double* vb = Vs + ((rb * 4 + gg + 1) * (IB / 8) + nb) * 64;
+            bn[0][nb] = vb[s1a];
+            bn[1][nb] = vb[s1b];
+            if (dg) {
+              bn[0][nb] = vmask(bn[0][nb], 8 * (gg + 1) + 2 * c, 8 * nb + r);
+              bn[1][nb] = vmask(bn[1][nb], 8 * (gg + 1) + 2 * c + 1, 8 * nb + r);
+            }
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) dmma(w[nb], x[rb * 4 + gg][h], bc[h][nb]);
+        pf();
+        if (gg < 3) {
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) {
+            bc[0][nb] = bn[0][nb];
+            bc[1][nb] = bn[1][nb];
+          }
+        }
       }
     }
   }
+  UPROF_MARK_V(10, _tq);
   // W^T <- W^T T (Q^T) or W^T T^T (Q); T upper triangular
+  double tb[2][4][4];
+#pragma unroll
+  for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb)
+      if (TRANST ? (kb <= nb) : (kb >= nb)) {
+        const double* tp = TRANST ? Ts + (kb * 4 + nb) * 64 : Ts + (nb * 4 + kb) * 64;
+        tb[0][kb][nb] = tp[TRANST ? s1a : s3a];
+        tb[1][kb][nb] = tp[TRANST ? s1b : s3b];
+      }
   double wt[4][2];
 #pragma unroll
   for (int nb = 0; nb < 4; ++nb) wt[nb][0] = wt[nb][1] = 0.0;
 #pragma unroll
   for (int kb = 0; kb < 4; ++kb)
 #pragma unroll
-    for (int nb = 0; nb < 4; ++nb) {
-      if (TRANST ? (kb <= nb) : (kb >= nb)) {
-        const double* tb = TRANST ? Ts + (kb * 4 + nb) * 64 : Ts + (nb * 4 + kb) * 64;
-        dmma(wt[nb], w[kb][0], tb[TRANST ? s1a : s3a]);
-        dmma(wt[nb], w[kb][1], tb[TRANST ? s1b : s3b]);
-      }
-    }
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb)
+        if (TRANST ? (kb <= nb) : (kb >= nb)) dmma(wt[nb], w[kb][h], tb[h][kb][nb]);
   if (top) {
 #pragma unroll
     for (int nb = 0; nb < 4; ++nb) stcg2(top + 8 * nb + 2 * c + r * NB, ap[nb][0] - wt[nb][0], ap[nb][1] - wt[nb][1]);
@@ -130,18 +238,54 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int g0, int g
     wt[nb][0] = -wt[nb][0];
     wt[nb][1] = -wt[nb][1];
   }
-  // X -= W^T V^T
+  UPROF_MARK_V(11, _tq);
+  // X -= W^T V^T ; consecutive DMMAs hit different row groups (independent)
 #pragma unroll
-  for (int g = 0; g < NB / 8; ++g) {
-    if (g >= g0 && g < g1) {
-      const double* vb = Vs + g * (IB / 8) * 64;
+  for (int rb = 0; rb < NB / IB; ++rb) {
+    if (rb >= rb0 && rb < rb1) {
+      const bool dg = (MASK != 2) && rb == drb;
+      double bc[2][4], bn[2][4];
+#pragma unroll
+      for (int gg = 0; gg < 4; ++gg) {
+        const double* vb = Vs + ((rb * 4 + gg) * (IB / 8)) * 64;
+        bc[0][gg] = vb[s3a];
+        bc[1][gg] = vb[s3b];
+        if (dg) {
+          bc[0][gg] = vmask(bc[0][gg], 8 * gg + r, 2 * c);
+          bc[1][gg] = vmask(bc[1][gg], 8 * gg + r, 2 * c + 1);
+        }
+      }
 #pragma unroll
       for (int kb = 0; kb < 4; ++kb) {
-        dmma(x[g], wt[kb][0], vb[kb * 64 + s3a]);
-        dmma(x[g], wt[kb][1], vb[kb * 64 + s3b]);
+        if (kb < 3) {
+#pragma unroll
+          for (int gg = 0; gg < 4; ++gg) {
+            const double* vb = Vs + ((rb * 4 + gg) * (IB / 8) + kb + 1) * 64;
+            bn[0][gg] = vb[s3a];
+            bn[1][gg] = vb[s3b];
+            if (dg) {
+              bn[0][gg] = vmask(bn[0][gg], 8 * gg + r, 8 * (kb + 1) + 2 * c);
+              bn[1][gg] = vmask(bn[1][gg], 8 * gg + r, 8 * (kb + 1) + 2 * c + 1);
+            }
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int gg = 0; gg < 4; ++gg) dmma(x[rb * 4 + gg], wt[kb][h], bc[h][gg]);
+        pf();
+        if (kb < 3) {
+#pragma unroll
+          for (int gg = 0; gg < 4; ++gg) {
+            bc[0][gg] = bn[0][gg];
+            bc[1][gg] = bn[1][gg];
+          }
+        }
       }
     }
   }
+  pf.flush();
+  UPROF_MARK_V(12, _tq);
 }
 
 // x rows [8*g0, 8*g1) of the warp's columns (column-major tile, ld NB)
@@ -167,47 +311,86 @@ __device__ __forceinline__ void store_x(const double (&x)[NB / 8][2], double* co
     if (g >= g0 && g < g1) stcg2(col + r * NB + 8 * g + 2 * c, x[g][0], x[g][1]);
 }
 
-// Stage block b of the reflectors of tile `vt` (ld NB) into swizzled smem,
-// rows [row0, row1), masking per mode: GE unit-lower (diag block), TT
-// upper-triangular, TS full.  Asynchronous (cp.async); masked entries are
-// written directly.  All threads participate.
-template <int NB, int MODE>
-__device__ __forceinline__ void stage_v(double* Vs, const double* __restrict__ vt, int b, int row0, int row1, int tid) {
-  const int warp = tid >> 5, lane = tid & 31;
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+// Producer staging (the NPW warps of the producer warpgroup, pw = 0..NPW-1).
+// Rows [row0, row1) of reflector block b of tile `vt` (ld NB) into swizzled
+// smem, 8-byte cp.async; one instruction covers 8 rows x 4 columns (16
+// distinct banks per half-warp, 64-byte global segments).  No masking: the
+// diagonal 32x32 block of a GE (unit-lower) / TT (upper) reflector block is
+// masked where the B fragments are read (warp_apply).
+constexpr int NPW = 4;
+template <int NB>
+__device__ __forceinline__ void pstage_v(double* Vs, const double* __restrict__ vt, int b, int row0, int row1, int pw,
+                                         int lane) {
   const int a = lane & 7, cq = lane >> 3;
-  const int col0 = b * IB;
-  const int units = ((row1 - row0) >> 3) * (IB / 4);
-  for (int u = warp; u < units; u += NW) {
-    const int row = row0 + (u / (IB / 4)) * 8 + a;
-    const int cl = (u % (IB / 4)) * 4 + cq;  // column within the block
-    const int col = col0 + cl;
-    double* dst = Vs + swz(row, cl);
-    if (MODE == GE) {
-      if (row > col)
-        cp_async8(dst, vt + row + size_t(col) * NB);
-      else
-        *dst = (row == col) ? 1.0 : 0.0;
-    } else if (MODE == TT) {
-      if (row <= col)
-        cp_async8(dst, vt + row + size_t(col) * NB);
-      else
-        *dst = 0.0;
-    } else {
-      cp_async8(dst, vt + row + size_t(col) * NB);
-    }
+  // unit u -> rows row0 + 8*(u>>3) + a, column 4*(u&7) + cq; this warp does
+  // u = pw + NPW*t, i.e. two fixed columns per warp (IB/4 == 2*NPW)
+  const int c0 = 4 * pw + cq, c1 = c0 + 4 * NPW;
+  const double* s0 = vt + size_t(b * IB + c0) * NB + row0 + a;
+  const double* s1 = vt + size_t(b * IB + c1) * NB + row0 + a;
+  double* d0 = Vs + (c0 >> 3) * 64 + swz_in(a, c0 & 7) + (row0 >> 3) * (IB / 8) * 64;
+  double* d1 = Vs + (c1 >> 3) * 64 + swz_in(a, c1 & 7) + (row0 >> 3) * (IB / 8) * 64;
+  for (int rr = 0; rr < row1 - row0; rr += 8) {
+    cp_async8(d0, s0 + rr);
+    cp_async8(d1, s1 + rr);
+    d0 += (IB / 8) * 64;
+    d1 += (IB / 8) * 64;
   }
 }
 
-// Stage T_b (IB x IB upper triangular; LAPACK ldt = IB) into swizzled smem.
-__device__ __forceinline__ void stage_t(double* Ts, const double* __restrict__ tt, int b, int tid) {
-  for (int e = tid; e < IB * IB; e += NT) {
-    const int row = e & (IB - 1), col = e / IB;  // row-fastest: coalesced
-    double* dst = Ts + swz(row, col);
-    if (row <= col)
-      cp_async8(dst, tt + row + size_t(b * IB + col) * IB);
-    else
-      *dst = 0.0;
+// T_b (IB x IB; LAPACK ldt = IB, lower part zero as written by the panels)
+__device__ __forceinline__ void pstage_t(double* Ts, const double* __restrict__ tt, int b, int pw, int lane) {
+  const int a = lane & 7, cq = lane >> 3;
+  const int c0 = 4 * pw + cq, c1 = c0 + 4 * NPW;
+#pragma unroll
+  for (int rr = 0; rr < IB; rr += 8) {
+    cp_async8(Ts + swz(rr + a, c0), tt + rr + a + size_t(b * IB + c0) * IB);
+    cp_async8(Ts + swz(rr + a, c1), tt + rr + a + size_t(b * IB + c1) * IB);
   }
 }
+
+// IB pivot rows [r0, r0+IB) of WS columns from col0 (ld NB) -> smem,
+// column-major ld IB, 16-byte copies
+template <int NB>
+__device__ __forceinline__ void pstage_top(double* dst, const double* __restrict__ tile, int col0, int r0, int pw,
+                                           int lane) {
+  for (int e = pw * 32 + lane; e < WS * (IB / 2); e += NPW * 32) {
+    const int cc = e / (IB / 2), rr = (e % (IB / 2)) * 2;
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst + rr + cc * IB));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(tile + size_t(col0 + cc) * NB + r0 + rr));
+  }
+}
+
+// ---- mbarrier helpers (producer/consumer handshake)
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+               "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared.b64 st, [%0];\n}\n" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+// arrive when all prior cp.async of this thread have landed
+__device__ __forceinline__ void mbar_arrive_cpasync(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];\n" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// barrier among the 8 compute warps only (the producer warp is elsewhere)
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 
 }  // namespace tqrk

@@ -16,102 +16,18 @@
 #include <cstdio>
 #include <map>
 #include <numeric>
+#include <queue>
 #include <string>
 #include <vector>
 
 #include "capi_internal.hpp"
-#include "tqr_tasks.cuh"
+#include "tqr_exec.cuh"
 
 using namespace tqrk;
 
+using namespace tqrx;
+
 namespace {
-
-struct Item {
-  int8_t kind;
-  int8_t slab;
-  int16_t pad;
-  int32_t i, piv, k, j;
-  int32_t pred_lo, pred_n;
-};
-static_assert(sizeof(Item) == 28, "item layout");
-
-struct ExecParams {
-  const Item* items;
-  const int32_t* preds;
-  int n_items;
-  int* done;
-  int* queue;
-  const double* vtiles;  // reflector source (factored tiles)
-  double* tiles;         // tiles the items write (== vtiles when factoring)
-  double* tg;
-  double* te;
-  int p;
-};
-
-template <int NB>
-__device__ __forceinline__ size_t toff(int p, int i, int j) {
-  return (size_t(j - 1) * size_t(p) + size_t(i - 1)) * size_t(NB) * NB;
-}
-template <int NB>
-__device__ __forceinline__ size_t soff(int p, int i, int k) {
-  return (size_t(k - 1) * size_t(p) + size_t(i - 1)) * size_t(IB) * NB;
-}
-
-template <int NB, bool TRANST>
-__global__ void __launch_bounds__(NT, 1) exec_kernel(ExecParams P) {
-  extern __shared__ __align__(16) double sm[];
-  __shared__ int s_item;
-  const int tid = threadIdx.x;
-  for (;;) {
-    if (tid == 0) s_item = atomicAdd(P.queue, 1);
-    __syncthreads();
-    const int it = s_item;
-    if (it >= P.n_items) break;
-    const Item I = P.items[it];
-    if (tid < 32) {
-      for (int t = tid; t < I.pred_n; t += 32) {
-        const int pr = P.preds[I.pred_lo + t];
-        while (ld_acquire(P.done + pr) == 0) __nanosleep(40);
-      }
-      __syncwarp();
-      __threadfence();  // gpu-scope fence: also drops stale L1 lines
-    }
-    __syncthreads();
-    switch (I.kind) {
-      case tqr::GEQRT:
-        if constexpr (TRANST)
-          panel_item<NB, GE>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), nullptr, P.tg + soff<NB>(P.p, I.i, I.k), tid);
-        break;
-      case tqr::TTQRT:
-        if constexpr (TRANST)
-          panel_item<NB, TT>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.k),
-                             P.te + soff<NB>(P.p, I.i, I.k), tid);
-        break;
-      case tqr::TSQRT:
-        if constexpr (TRANST)
-          panel_item<NB, TS>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.k),
-                             P.te + soff<NB>(P.p, I.i, I.k), tid);
-        break;
-      case tqr::UNMQR:
-        update_item<NB, GE, TRANST>(sm, P.vtiles + toff<NB>(P.p, I.i, I.k), P.tg + soff<NB>(P.p, I.i, I.k),
-                                    P.tiles + toff<NB>(P.p, I.i, I.j), nullptr, I.slab, tid);
-        break;
-      case tqr::TTMQR:
-        update_item<NB, TT, TRANST>(sm, P.vtiles + toff<NB>(P.p, I.i, I.k), P.te + soff<NB>(P.p, I.i, I.k),
-                                    P.tiles + toff<NB>(P.p, I.i, I.j), P.tiles + toff<NB>(P.p, I.piv, I.j), I.slab,
-                                    tid);
-        break;
-      case tqr::TSMQR:
-        update_item<NB, TS, TRANST>(sm, P.vtiles + toff<NB>(P.p, I.i, I.k), P.te + soff<NB>(P.p, I.i, I.k),
-                                    P.tiles + toff<NB>(P.p, I.i, I.j), P.tiles + toff<NB>(P.p, I.piv, I.j), I.slab,
-                                    tid);
-        break;
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) st_release(P.done + it, 1);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // pack / unpack / R extraction (HBM-bound copies through a 32x33 smem tile)
@@ -205,6 +121,13 @@ struct Task {
   int32_t i, piv, k, j;
 };
 
+int num_sms_host() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+  return sms > 0 ? sms : 148;
+}
+
 inline bool is_update(int kind) { return kind == tqr::UNMQR || kind == tqr::TTMQR || kind == tqr::TSMQR; }
 
 // tasks in execution order + incoming task edges -> slab items + pred CSR
@@ -250,6 +173,93 @@ void expand(const std::vector<Task>& tasks, const std::vector<std::vector<int32_
   }
 }
 
+// Device-realistic relative cost of one work item (an update slab = 1).
+inline double item_cost(int kind, int nb) {
+  const double big = nb >= 256 ? 1.0 : 0.5;
+  switch (kind) {
+    case tqr::GEQRT: return 3.0 * big + 0.5;
+    case tqr::TTQRT: return 2.5 * big + 0.5;
+    case tqr::TSQRT: return 4.0 * big + 0.5;
+    case tqr::TSMQR: return 2.0;
+    default: return 1.0;
+  }
+}
+
+// Reorder items into the start order of a simulated list schedule on
+// `workers` SMs with Backflow priorities (longest weighted path to the end,
+// taskgraph.py:338-362) and lowest-id tie break, the MaxCP policy of the
+// reference's list scheduler (sched.py:77-156).  The result is a
+// topological order, which the executor's deadlock-freedom needs.
+void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers, int nb) {
+  const size_t n = items.size();
+  if (n == 0) return;
+  std::vector<int32_t> nsucc(n + 1, 0);
+  for (size_t v = 0; v < n; ++v)
+    for (int32_t k = 0; k < items[v].pred_n; ++k) nsucc[size_t(preds[size_t(items[v].pred_lo + k)]) + 1]++;
+  for (size_t v = 0; v < n; ++v) nsucc[v + 1] += nsucc[v];
+  std::vector<int32_t> succ(static_cast<size_t>(nsucc[n]));
+  std::vector<int32_t> fill(nsucc.begin(), nsucc.end() - 1);
+  for (size_t v = 0; v < n; ++v)
+    for (int32_t k = 0; k < items[v].pred_n; ++k) {
+      const int32_t u = preds[size_t(items[v].pred_lo + k)];
+      succ[size_t(fill[size_t(u)]++)] = int32_t(v);
+    }
+  std::vector<double> w(n), prio(n, 0.0);
+  for (size_t v = 0; v < n; ++v) w[v] = item_cost(items[v].kind, nb);
+  for (size_t v = n; v-- > 0;) {  // items are in a topological order already
+    double best = 0.0;
+    for (int32_t k = nsucc[v]; k < nsucc[v + 1]; ++k) best = std::max(best, prio[size_t(succ[size_t(k)])]);
+    prio[v] = w[v] + best;
+  }
+  std::vector<int32_t> indeg(n);
+  for (size_t v = 0; v < n; ++v) indeg[v] = items[v].pred_n;
+  using RQ = std::pair<double, int32_t>;  // (-priority, id) min-heap == max priority, lowest id
+  std::priority_queue<RQ, std::vector<RQ>, std::greater<RQ>> ready;
+  for (size_t v = 0; v < n; ++v)
+    if (indeg[v] == 0) ready.emplace(-prio[v], int32_t(v));
+  using EV = std::pair<double, int32_t>;  // (finish time, id)
+  std::priority_queue<EV, std::vector<EV>, std::greater<EV>> running;
+  std::vector<int32_t> order;
+  order.reserve(n);
+  double now = 0.0;
+  int idle = workers;
+  while (order.size() < n) {
+    while (idle > 0 && !ready.empty()) {
+      const int32_t v = ready.top().second;
+      ready.pop();
+      order.push_back(v);
+      running.emplace(now + w[size_t(v)], v);
+      --idle;
+    }
+    if (running.empty()) break;  // cannot happen for a DAG
+    now = running.top().first;
+    while (!running.empty() && running.top().first <= now) {
+      const int32_t u = running.top().second;
+      running.pop();
+      ++idle;
+      for (int32_t k = nsucc[size_t(u)]; k < nsucc[size_t(u) + 1]; ++k) {
+        const int32_t v = succ[size_t(k)];
+        if (--indeg[size_t(v)] == 0) ready.emplace(-prio[size_t(v)], v);
+      }
+    }
+  }
+  if (order.size() != n) throw std::runtime_error("cp_order: dependency cycle");
+  std::vector<int32_t> pos(n);
+  for (size_t t = 0; t < n; ++t) pos[size_t(order[t])] = int32_t(t);
+  std::vector<Item> ni(n);
+  std::vector<int32_t> np;
+  np.reserve(preds.size());
+  for (size_t t = 0; t < n; ++t) {
+    Item it = items[size_t(order[t])];
+    const int32_t lo = it.pred_lo;
+    it.pred_lo = int32_t(np.size());
+    for (int32_t k = 0; k < it.pred_n; ++k) np.push_back(pos[size_t(preds[size_t(lo + k)])]);
+    ni[t] = it;
+  }
+  items.swap(ni);
+  preds.swap(np);
+}
+
 void upload(DevSched& d, const std::vector<Item>& items, const std::vector<int32_t>& preds) {
   d.n_items = int(items.size());
   d.n_preds = int64_t(preds.size());
@@ -281,6 +291,8 @@ struct tqr_plan {
 
 namespace {
 
+unsigned long long* g_trace = nullptr;  // tqr_set_trace: per-item timestamps of the next run
+
 int num_sms() {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -288,38 +300,24 @@ int num_sms() {
   return sms > 0 ? sms : 148;
 }
 
-template <int NB, bool TRANST>
-cudaError_t launch_exec(const DevSched& d, const double* vtiles, double* tiles, double* tg, double* te, int p,
-                        cudaStream_t st) {
-  auto kern = exec_kernel<NB, TRANST>;
-  const size_t smem = Smem<NB>::BYTES;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
+cudaError_t run(const DevSched& d, int nb, bool transT, const double* vtiles, double* tiles, double* tg, double* te,
+                int p, cudaStream_t st) {
+  cudaError_t e;
   if ((e = cudaMemsetAsync(d.done, 0, size_t(std::max(d.n_items, 1)) * sizeof(int), st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(d.queue, 0, sizeof(int), st)) != cudaSuccess) return e;
   if (d.n_items == 0) return cudaSuccess;
-  ExecParams P{d.items, d.preds, d.n_items, d.done, d.queue, vtiles, tiles, tg, te, p};
+  DevView v{d.items, d.preds, d.done, d.queue, d.n_items};
   const int grid = std::min(d.n_items, num_sms());
-  kern<<<grid, NT, smem, st>>>(P);
-  return cudaGetLastError();
-}
-
-cudaError_t run(const DevSched& d, int nb, bool transT, const double* vtiles, double* tiles, double* tg, double* te,
-                int p, cudaStream_t st) {
   switch (nb) {
     case 64:
-      return transT ? launch_exec<64, true>(d, vtiles, tiles, tg, te, p, st)
-                    : launch_exec<64, false>(d, vtiles, tiles, tg, te, p, st);
-    case 128:
-      return transT ? launch_exec<128, true>(d, vtiles, tiles, tg, te, p, st)
-                    : launch_exec<128, false>(d, vtiles, tiles, tg, te, p, st);
+      return transT ? launch_exec<64, true>(v, vtiles, tiles, tg, te, p, g_trace, grid, st)
+                    : launch_exec<64, false>(v, vtiles, tiles, tg, te, p, g_trace, grid, st);
     case 256:
-      return transT ? launch_exec<256, true>(d, vtiles, tiles, tg, te, p, st)
-                    : launch_exec<256, false>(d, vtiles, tiles, tg, te, p, st);
+      return transT ? launch_exec<256, true>(v, vtiles, tiles, tg, te, p, g_trace, grid, st)
+                    : launch_exec<256, false>(v, vtiles, tiles, tg, te, p, g_trace, grid, st);
   }
   return cudaErrorInvalidValue;
 }
-
 
 int cuda_guarded(cudaError_t e) {
   if (e == cudaSuccess) return TQR_OK;
@@ -336,7 +334,7 @@ int tqr_plan_create(const tqr_build* hb, int nb, int ib, tqr_plan** out) {
     if (!hb || !hb->b) throw tqr::ValueError("null build");
     const tqr::Build& b = *hb->b;
     if (!b.keep_trace) throw tqr::ValueError("plan needs a build made with keep_trace=True");
-    if (nb != 64 && nb != 128 && nb != 256) throw tqr::ValueError("nb must be 64, 128 or 256");
+    if (nb != 64 && nb != 256) throw tqr::ValueError("nb must be 64 or 256");
     if (ib != IB) throw tqr::ValueError("ib must be 32");
     auto* P = new tqr_plan;
     try {
@@ -374,6 +372,7 @@ int tqr_plan_create(const tqr_build* hb, int nb, int ib, tqr_plan** out) {
       std::vector<Item> items;
       std::vector<int32_t> preds;
       expand(P->trace, in, order, nb / WS, items, preds);
+      cp_order(items, preds, num_sms_host(), nb);
       upload(P->fac, items, preds);
       const double m = double(b.p) * nb, nn = double(b.q) * nb;
       P->flops = 2.0 * nn * nn * (m - nn / 3.0);
@@ -460,6 +459,7 @@ int tqr_apply_q(tqr_plan* P, int trans, const double* tiles, const double* tg, c
     std::vector<Item> items;
     std::vector<int32_t> preds;
     expand(tasks, in, order, P->nb / WS, items, preds);
+    cp_order(items, preds, num_sms_host(), P->nb);
     DevSched d;
     upload(d, items, preds);
     P->aq[key] = d;
@@ -498,6 +498,27 @@ int tqr_extract_r(const double* tiles, int p, int q, int nb, double* R, int64_t 
     unpack_kernel<<<unsigned(blocks_j), 256, 0, st>>>(col, q, 1, nb, dst, ldr, row_major, 1, int64_t(j) * nb);
   }
   return cuda_guarded(cudaGetLastError());
+}
+
+int tqr_set_trace(void* trace_dev) {
+  g_trace = static_cast<unsigned long long*>(trace_dev);
+  return TQR_OK;
+}
+
+int tqr_plan_items(const tqr_plan* P, int32_t* out7) {
+  // (kind, slab, i, piv, k, j, n_preds) per factorization item, device order
+  return tqr::guard([&] {
+    std::vector<Item> items(size_t(P->fac.n_items));
+    if (!items.empty()) {
+      cudaError_t e = cudaMemcpy(items.data(), P->fac.items, items.size() * sizeof(Item), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    }
+    for (size_t t = 0; t < items.size(); ++t) {
+      const Item& I = items[t];
+      int32_t* o = out7 + 7 * t;
+      o[0] = I.kind; o[1] = I.slab; o[2] = I.i; o[3] = I.piv; o[4] = I.k; o[5] = I.j; o[6] = I.pred_n;
+    }
+  });
 }
 
 int tqr_fp64_peak(double* tflops_out, void* stream) {

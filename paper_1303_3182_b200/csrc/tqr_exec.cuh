@@ -1,0 +1,233 @@
+// Persistent dataflow executor (device side), shared by the per-(nb, trans)
+// translation units tqr_exec_<nb><t|n>.cu so they compile in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "sched.hpp"
+#include "tqr_tasks.cuh"
+
+using namespace tqrk;
+
+namespace tqrx {
+
+struct Item {
+  int8_t kind;
+  int8_t slab;
+  int16_t pad;
+  int32_t i, piv, k, j;
+  int32_t pred_lo, pred_n;
+};
+static_assert(sizeof(Item) == 28, "item layout");
+
+struct ExecParams {
+  const Item* items;
+  const int32_t* preds;
+  int n_items;
+  int* done;
+  int* queue;
+  const double* vtiles;  // reflector source (factored tiles)
+  double* tiles;         // tiles the items write (== vtiles when factoring)
+  double* tg;
+  double* te;
+  int p;
+  unsigned long long* trace;  // optional: per item {t_dequeue, t_ready, t_end, smid}
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+  return s;
+}
+
+template <int NB>
+__device__ __forceinline__ size_t toff(int p, int i, int j) {
+  return (size_t(j - 1) * size_t(p) + size_t(i - 1)) * size_t(NB) * NB;
+}
+template <int NB>
+__device__ __forceinline__ size_t soff(int p, int i, int k) {
+  return (size_t(k - 1) * size_t(p) + size_t(i - 1)) * size_t(IB) * NB;
+}
+
+// L2 prefetch of the tiles the next work item will touch (its data tiles;
+// reflector tiles are shared by many items and usually resident).
+template <int NB>
+__device__ __forceinline__ void prefetch_item(const ExecParams& P, const Item& I) {
+  const unsigned tile_bytes = unsigned(NB) * NB * sizeof(double);
+  const unsigned slab_bytes = unsigned(WS) * NB * sizeof(double);
+  switch (I.kind) {
+    case tqr::GEQRT:
+      prefetch_l2(P.tiles + toff<NB>(P.p, I.i, I.k), tile_bytes);
+      break;
+    case tqr::TTQRT:
+    case tqr::TSQRT:
+      prefetch_l2(P.tiles + toff<NB>(P.p, I.i, I.k), tile_bytes);
+      prefetch_l2(P.tiles + toff<NB>(P.p, I.piv, I.k), tile_bytes);
+      break;
+    case tqr::UNMQR:
+      prefetch_l2(P.tiles + toff<NB>(P.p, I.i, I.j) + size_t(I.slab) * WS * NB, slab_bytes);
+      break;
+    default:
+      prefetch_l2(P.tiles + toff<NB>(P.p, I.i, I.j) + size_t(I.slab) * WS * NB, slab_bytes);
+      prefetch_l2(P.tiles + toff<NB>(P.p, I.piv, I.j) + size_t(I.slab) * WS * NB, slab_bytes);
+      break;
+  }
+}
+
+__device__ __forceinline__ bool is_update_kind(int k) { return k == tqr::UNMQR || k == tqr::TTMQR || k == tqr::TSMQR; }
+
+// Warp-specialized persistent executor.  Warpgroups 0-1 (8 warps, 232
+// registers) run the kernels; warpgroup 2 (40 registers) stages reflector
+// blocks for update items (warp 8) and prefetches the next item's tiles into
+// L2 (warp 9).  Per item both roles pass the same three CTA barriers.
+template <int NB, bool TRANST>
+__global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_cur, s_nxt;
+  __shared__ __align__(8) unsigned long long bars[4];  // full[2], empty[2]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // each CTA holds one dequeued item ahead (deadlock-free: items are taken in
+  // a topological order and an item only waits on lower-numbered ones)
+  if (tid == 0) {
+    mbar_init(&bars[0], 32 * NPW);
+    mbar_init(&bars[1], 32 * NPW);
+    mbar_init(&bars[2], NW);
+    mbar_init(&bars[3], NW);
+    s_cur = atomicAdd(P.queue, 1);
+    s_nxt = s_cur < P.n_items ? atomicAdd(P.queue, 1) : P.n_items;
+  }
+  bar_all();
+  unsigned seq = 0;
+  constexpr unsigned NBLK = NB / IB;
+  if (warp >= NW) {
+    setmaxnreg_dec<40>();
+    for (;;) {
+      const int it = s_cur, nx = s_nxt;
+      if (it >= P.n_items) break;
+      const Item I = P.items[it];
+      bar_all();  // dependencies satisfied
+      if (warp == NW && lane == 0 && nx < P.n_items) prefetch_item<NB>(P, P.items[nx]);
+      if (is_update_kind(I.kind)) {
+        const int pw = warp - NW;
+        const double* vt = P.vtiles + toff<NB>(P.p, I.i, I.k);
+        if (I.kind == tqr::UNMQR)
+          update_produce<NB, GE, TRANST>(sm, vt, P.tg + soff<NB>(P.p, I.i, I.k), nullptr, I.slab, pw, lane, bars,
+                                         bars + 2, seq);
+        else if (I.kind == tqr::TTMQR)
+          update_produce<NB, TT, TRANST>(sm, vt, P.te + soff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.j),
+                                         I.slab, pw, lane, bars, bars + 2, seq);
+        else
+          update_produce<NB, TS, TRANST>(sm, vt, P.te + soff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.j),
+                                         I.slab, pw, lane, bars, bars + 2, seq);
+      }
+      if (is_update_kind(I.kind)) seq += NBLK;
+      bar_all();  // item finished
+      bar_all();  // next item published
+    }
+    return;
+  }
+  setmaxnreg_inc<232>();
+  for (;;) {
+    const int it = s_cur, nx = s_nxt;
+    if (it >= P.n_items) break;
+    const Item I = P.items[it];
+    unsigned long long t_deq = 0;
+    if (P.trace && tid == 0) t_deq = gtimer();
+    if (warp == 0) {
+      for (int t = lane; t < I.pred_n; t += 32) {
+        const int pr = P.preds[I.pred_lo + t];
+        while (ld_acquire(P.done + pr) == 0) __nanosleep(40);
+      }
+      __syncwarp();
+      __threadfence();  // gpu-scope fence: also drops stale L1 lines
+    }
+    bar_all();
+    unsigned long long t_rdy = 0;
+    if (P.trace && tid == 0) t_rdy = gtimer();
+    unsigned long long* pprof = P.trace ? P.trace + 4 * size_t(P.n_items) : nullptr;
+    switch (I.kind) {
+      case tqr::GEQRT:
+        if constexpr (TRANST)
+          panel_item<NB, GE>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), nullptr, P.tg + soff<NB>(P.p, I.i, I.k), tid, pprof);
+        break;
+      case tqr::TTQRT:
+        if constexpr (TRANST)
+          panel_item<NB, TT>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.k),
+                             P.te + soff<NB>(P.p, I.i, I.k), tid, pprof);
+        break;
+      case tqr::TSQRT:
+        if constexpr (TRANST)
+          panel_item<NB, TS>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.k),
+                             P.te + soff<NB>(P.p, I.i, I.k), tid, pprof);
+        break;
+      case tqr::UNMQR:
+        update_consume<NB, GE, TRANST>(sm, P.tiles + toff<NB>(P.p, I.i, I.j), nullptr, I.slab, tid, bars, bars + 2,
+                                       seq);
+        break;
+      case tqr::TTMQR:
+        update_consume<NB, TT, TRANST>(sm, P.tiles + toff<NB>(P.p, I.i, I.j), P.tiles + toff<NB>(P.p, I.piv, I.j),
+                                       I.slab, tid, bars, bars + 2, seq);
+        break;
+      case tqr::TSMQR:
+        update_consume<NB, TS, TRANST>(sm, P.tiles + toff<NB>(P.p, I.i, I.j), P.tiles + toff<NB>(P.p, I.piv, I.j),
+                                       I.slab, tid, bars, bars + 2, seq);
+        break;
+    }
+    if (is_update_kind(I.kind)) seq += NBLK;
+    __threadfence();
+    bar_all();
+    if (tid == 0) {
+      st_release(P.done + it, 1);
+      if (P.trace) {
+        P.trace[4 * size_t(it)] = t_deq;
+        P.trace[4 * size_t(it) + 1] = t_rdy;
+        P.trace[4 * size_t(it) + 2] = gtimer();
+        P.trace[4 * size_t(it) + 3] = smid();
+      }
+      s_cur = nx;
+      s_nxt = nx < P.n_items ? atomicAdd(P.queue, 1) : P.n_items;
+    }
+    bar_all();
+  }
+}
+
+struct DevView {
+  const Item* items;
+  const int32_t* preds;
+  int* done;
+  int* queue;
+  int n_items;
+};
+
+template <int NB, bool TRANST>
+cudaError_t launch_exec(const DevView& d, const double* vtiles, double* tiles, double* tg, double* te, int p,
+                        unsigned long long* trace, int grid, cudaStream_t st);
+
+// specializations live in tqr_exec_<nb><t|n>.cu
+#define TQR_DECLARE_LAUNCH(NB, TR)                                                                                  \
+  template <>                                                                                                      \
+  cudaError_t launch_exec<NB, TR>(const DevView& d, const double* vtiles, double* tiles, double* tg, double* te,  \
+                                  int p, unsigned long long* trace, int grid, cudaStream_t st);
+TQR_DECLARE_LAUNCH(64, true)
+TQR_DECLARE_LAUNCH(64, false)
+TQR_DECLARE_LAUNCH(256, true)
+TQR_DECLARE_LAUNCH(256, false)
+
+#define TQR_DEFINE_LAUNCH(NB, TR)                                                                                   \
+  template <>                                                                                                      \
+  cudaError_t launch_exec<NB, TR>(const DevView& d, const double* vtiles, double* tiles, double* tg, double* te,  \
+                                  int p, unsigned long long* trace, int grid, cudaStream_t st) {                   \
+    auto kern = exec_kernel<NB, TR>;                                                                               \
+    const size_t smem = Smem<NB>::BYTES;                                                                           \
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));            \
+    if (e != cudaSuccess) return e;                                                                                \
+    ExecParams P{d.items, d.preds, d.n_items, d.done, d.queue, vtiles, tiles, tg, te, p, trace};                   \
+    kern<<<grid, NTP, smem, st>>>(P);                                                                               \
+    return cudaGetLastError();                                                                                     \
+  }
+
+}  // namespace tqrx

@@ -8,219 +8,298 @@
 
 namespace tqrk {
 
-// Shared-memory carve-up (doubles).  Update items: Vs[2] + Ts[2].
-// Panel items: P (stacked panel), Vs, Ts, G and per-column scalars.
+// Shared-memory carve-up (doubles).  Update items: Vs[2] + Ts[2] + pivot rows[2].
+// Panel items: top block, staged V/T for the trailing update, Gram column
+// store, reduction partials, diagonal-row / s broadcasts, per-column scalars.
 template <int NB>
 struct Smem {
   static constexpr int VS = NB * IB;  // one staged V block
   static constexpr int TS = IB * IB;
-  static constexpr int PLD = NB + IB;  // panel leading dimension
-  static constexpr int P = PLD * IB;
   // update layout
-  static constexpr int U_V0 = 0, U_V1 = VS, U_T0 = 2 * VS, U_T1 = 2 * VS + TS, U_END = 2 * VS + 2 * TS;
+  static constexpr int TOP = IB * WS;  // staged pivot rows of a slab (TT/TS)
+  static constexpr int U_V0 = 0, U_V1 = VS, U_T0 = 2 * VS, U_T1 = 2 * VS + TS, U_P0 = 2 * VS + 2 * TS,
+                       U_P1 = U_P0 + TOP, U_END = U_P1 + TOP;
   // panel layout
-  static constexpr int P_P = 0, P_V = P, P_T = P + VS, P_G = P + VS + TS, P_SC = P + VS + 2 * TS;
-  static constexpr int P_END = P_SC + 4 * IB + 8;
+  static constexpr int P_TOP = 0, P_V = TS, P_T = P_V + VS, P_G = P_T + TS, P_PART = P_G + TS;
+  static constexpr int P_DROW = P_PART + NW * IB, P_SBUF = P_DROW + IB, P_SC = P_SBUF + IB;
+  static constexpr int P_END = P_SC + 3 * IB + 8;
   static constexpr int END = U_END > P_END ? U_END : P_END;
   static constexpr size_t BYTES = size_t(END) * sizeof(double);
 };
+
+// After the call lane l holds the warp-wide sum of d[l] (recursive halving).
+__device__ __forceinline__ double warp_reduce_scatter32(double (&d)[32], int lane) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool up = lane & off;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      const double send = up ? d[i] : d[i + off];
+      const double keep = up ? d[i + off] : d[i];
+      d[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return d[0];
+}
 
 // ---------------------------------------------------------------------------
 // update item: apply all ib-blocks of one factor's reflectors to a 64-column
 // slab of the target tile(s), slab resident in registers for all blocks.
 
+template <int NB, int MODE>
+__device__ __forceinline__ void upd_rows(int b, int& r0, int& r1) {
+  if (MODE == GE) {
+    r0 = b * IB;
+    r1 = NB;
+  } else if (MODE == TT) {
+    r0 = 0;
+    r1 = (b + 1) * IB;
+  } else {
+    r0 = 0;
+    r1 = NB;
+  }
+}
+
+// Producer side of an update item (the NPW producer warps): stage V_b, T_b and the pivot
+// rows of every block into the double buffer, running ahead of the compute
+// warps (full/empty mbarriers; `seq` numbers staged blocks CTA-wide).
 template <int NB, int MODE, bool TRANST>
-__device__ void update_item(double* sm, const double* __restrict__ vt, const double* __restrict__ tt, double* xt,
-                            double* topt, int slab, int tid) {
+__device__ void update_produce(double* sm, const double* __restrict__ vt, const double* __restrict__ tt,
+                               const double* topt, int slab, int pw, int lane, unsigned long long* full,
+                               unsigned long long* empty, unsigned seq) {
   using S = Smem<NB>;
+  constexpr int NBLK = NB / IB;
+  const int scol0 = slab * WS;
+  for (int s = 0; s < NBLK; ++s) {
+    const unsigned q = seq + unsigned(s), buf = q & 1u;
+    if (q >= 2) mbar_wait(&empty[buf], ((q >> 1) - 1u) & 1u);
+    const int b = TRANST ? s : NBLK - 1 - s;
+    int r0, r1;
+    upd_rows<NB, MODE>(b, r0, r1);
+    pstage_v<NB>(sm + (buf ? S::U_V1 : S::U_V0), vt, b, r0, r1, pw, lane);
+    pstage_t(sm + (buf ? S::U_T1 : S::U_T0), tt, b, pw, lane);
+    if (MODE != GE) pstage_top<NB>(sm + (buf ? S::U_P1 : S::U_P0), topt, scol0, b * IB, pw, lane);
+    mbar_arrive_cpasync(&full[buf]);
+  }
+}
+
+// Compute side (8 warps): the warp's 8 columns of the slab stay in
+// registers while all ib-blocks are applied.
+template <int NB, int MODE, bool TRANST>
+__device__ void update_consume(double* sm, double* xt, double* topt, int slab, int tid, unsigned long long* full,
+                               unsigned long long* empty, unsigned seq) {
+  using S = Smem<NB>;
+  constexpr int NBLK = NB / IB;
   const int warp = tid >> 5, lane = tid & 31;
+  UPROF_DECL;
   const int col0 = slab * WS + warp * 8;
   double x[NB / 8][2];
   load_x<NB>(x, xt + size_t(col0) * NB, 0, NB / 8, lane);
-  constexpr int NBLK = NB / IB;
-  auto rows_of = [](int b, int& r0, int& r1) {
-    if (MODE == GE) {
-      r0 = b * IB;
-      r1 = NB;
-    } else if (MODE == TT) {
-      r0 = 0;
-      r1 = (b + 1) * IB;
-    } else {
-      r0 = 0;
-      r1 = NB;
-    }
-  };
-  {
-    const int b = TRANST ? 0 : NBLK - 1;
-    int r0, r1;
-    rows_of(b, r0, r1);
-    stage_v<NB, MODE>(sm + S::U_V0, vt, b, r0, r1, tid);
-    stage_t(sm + S::U_T0, tt, b, tid);
-    cp_async_commit();
-  }
+  UPROF_MARK(8);
   for (int s = 0; s < NBLK; ++s) {
+    const unsigned q = seq + unsigned(s), buf = q & 1u;
     const int b = TRANST ? s : NBLK - 1 - s;
-    if (s + 1 < NBLK) {
-      const int bn = TRANST ? s + 1 : NBLK - 2 - s;
-      int r0, r1;
-      rows_of(bn, r0, r1);
-      stage_v<NB, MODE>(sm + (((s + 1) & 1) ? S::U_V1 : S::U_V0), vt, bn, r0, r1, tid);
-      stage_t(sm + (((s + 1) & 1) ? S::U_T1 : S::U_T0), tt, bn, tid);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
+    mbar_wait(&full[buf], (q >> 1) & 1u);
+    UPROF_MARK(0);
     int r0, r1;
-    rows_of(b, r0, r1);
-    const double* Vs = sm + ((s & 1) ? S::U_V1 : S::U_V0);
-    const double* Ts = sm + ((s & 1) ? S::U_T1 : S::U_T0);
+    upd_rows<NB, MODE>(b, r0, r1);
+    const double* Vs = sm + (buf ? S::U_V1 : S::U_V0);
+    const double* Ts = sm + (buf ? S::U_T1 : S::U_T0);
     double* top = (MODE == GE) ? nullptr : topt + size_t(col0) * NB + b * IB;
-    warp_apply<NB, TRANST>(x, r0 / 8, r1 / 8, Vs, Ts, top, lane);
-    __syncthreads();
+    const double* top_s = (MODE == GE) ? nullptr : sm + (buf ? S::U_P1 : S::U_P0) + warp * 8 * IB;
+    warp_apply<NB, TRANST, MODE>(x, r0 / IB, r1 / IB, Vs, Ts, top, lane, top_s, b);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[buf]);
+    UPROF_MARK(2);
   }
   store_x<NB>(x, xt + size_t(col0) * NB, 0, NB / 8, lane);
+  UPROF_MARK(6);
 }
 
 // ---------------------------------------------------------------------------
 // panel item: Householder QR of one tile (GE), of [R_piv; R_i] (TT) or of
-// [R_piv; A_i] (TS), ib columns at a time: level-2 sweep of the block in
-// shared memory (warp-shuffle reductions), T_b from the Gram matrix, then
-// the block reflector applied to the trailing columns on DMMA.
+// [R_piv; A_i] (TS), ib columns at a time.  Level-2 sweep of a block with
+// one panel row per thread held in registers: per column a single 32-wide
+// warp reduce-scatter yields the column norm, the dots with the trailing
+// columns (the reflector application) and the dots with the previous
+// reflectors (the Gram column that builds T) — two CTA barriers per column.
+// Then T_b (dlarft recurrence) and the block reflector applied to the
+// trailing columns on DMMA.
 
+__device__ __forceinline__ unsigned long long ptimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// prof (optional, diagnostics): ns accumulated per phase
+// [0 load, 1 level-2, 2 write-back/stage, 3 T, 4 trailing update] + MODE*8
 template <int NB, int MODE>
 __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile (i,k)*/,
-                           double* rt /*TT/TS: pivot tile (piv,k)*/, double* tslot, int tid) {
+                           double* rt /*TT/TS: pivot tile (piv,k)*/, double* tslot, int tid,
+                           unsigned long long* prof = nullptr) {
+  unsigned long long tp = (prof && tid == 0) ? ptimer() : 0;
+  auto mark = [&](int ph) {
+    if (prof && tid == 0) {
+      const unsigned long long t2 = ptimer();
+      atomicAdd(prof + MODE * 8 + ph, t2 - tp);
+      tp = t2;
+    }
+  };
   using S = Smem<NB>;
-  constexpr int PLD = S::PLD;
   const int warp = tid >> 5, lane = tid & 31;
-  double* P = sm + S::P_P;
+  double* Ptop = sm + S::P_TOP;  // TT/TS: top block, column-major ld IB
   double* Vs = sm + S::P_V;
   double* Ts = sm + S::P_T;
-  double* G = sm + S::P_G;
+  double* G = sm + S::P_G;  // G[i + j*IB] = v_i . v_j, i < j
+  double* part = sm + S::P_PART;
+  double* drow = sm + S::P_DROW;
+  double* sbuf = sm + S::P_SBUF;
   double* tau_s = sm + S::P_SC;
   double* scal_s = tau_s + IB;
   double* beta_s = tau_s + 2 * IB;
-  double* nrm2_s = tau_s + 3 * IB;
+  const int t = tid;
 
   for (int b = 0; b < NB / IB; ++b) {
     const int rb0 = b * IB;
-    // rows of the stacked panel and the vector rows of column j
-    const int nrow = (MODE == GE) ? NB - rb0 : (MODE == TT ? IB + rb0 + IB : IB + NB);
-    auto vlo = [&](int j) { return MODE == GE ? j + 1 : IB; };
-    auto vhi = [&](int j) { return MODE == GE ? nrow : (MODE == TT ? IB + rb0 + j + 1 : nrow); };
-
-    // ---- load the panel block into P
+    // thread t owns panel row t: GE tile row rb0+t; TT/TS bottom-tile row t
+    const int nrows = (MODE == GE) ? NB - rb0 : (MODE == TT ? rb0 + IB : NB);
+    const bool own = t < nrows;
+    double row[IB];
+#pragma unroll
+    for (int c = 0; c < IB; ++c) {
+      double v = 0.0;
+      if (own) {
+        if (MODE == GE)
+          v = __ldcg(at + (rb0 + t) + size_t(rb0 + c) * NB);
+        else if (MODE == TS || t <= rb0 + c)
+          v = __ldcg(at + t + size_t(rb0 + c) * NB);
+      }
+      row[c] = v;
+    }
+    if (MODE != GE) {
+      for (int e = tid; e < IB * IB; e += NT) {
+        const int r = e % IB, c = e / IB;
+        Ptop[e] = (r <= c) ? __ldcg(rt + (rb0 + r) + size_t(rb0 + c) * NB) : 0.0;
+      }
+    }
+    csync();
+    mark(0);
+    // ---- level-2 sweep (dgeqr2 / dtpqrt2 semantics, LAPACK dlarfg).  A
+    // runtime loop (small code: the unrolled version is I-cache bound); the
+    // register row is indexed statically under predicates.
+#pragma unroll 1
+    for (int j = 0; j < IB; ++j) {
+      if (MODE == GE && t == j) {
+#pragma unroll
+        for (int c = 0; c < IB; ++c) drow[c] = row[c];
+      }
+      const bool inv = (MODE == GE) ? (own && t > j) : (MODE == TT ? (t <= rb0 + j) : own);
+      double xj = 0.0;
+#pragma unroll
+      for (int c = 0; c < IB; ++c) xj = (c == j) ? row[c] : xj;
+      const double x = inv ? xj : 0.0;
+      double d[IB];
+#pragma unroll
+      for (int c = 0; c < IB; ++c) d[c] = x * row[c];
+      part[warp * IB + lane] = warp_reduce_scatter32(d, lane);
+      csync();
+      if (warp == 0) {
+        double D = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) D += part[w * IB + lane];
+        const double alpha = (MODE == GE) ? drow[j] : Ptop[j + j * IB];
+        const double xn2 = __shfl_sync(0xffffffffu, D, j);
+        double tau = 0.0, scal = 0.0, beta = alpha;
+        if (xn2 != 0.0) {
+          beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+          const double rb = 1.0 / beta;
+          tau = (beta - alpha) * rb;
+          scal = 1.0 / (alpha - beta);
+        }
+        const double dr = (MODE == GE) ? drow[lane] : Ptop[j + lane * IB];
+        if (lane > j) {
+          const double sc = tau * (dr + scal * D);
+          sbuf[lane] = sc;
+          if (MODE != GE) Ptop[j + lane * IB] = dr - sc;
+        }
+        if (lane < j) G[lane + j * IB] = scal * D + ((MODE == GE) ? dr : 0.0);
+        if (MODE != GE && lane == j) Ptop[j + j * IB] = beta;
+        if (lane == 0) {
+          tau_s[j] = tau;
+          scal_s[j] = scal;
+          beta_s[j] = beta;
+        }
+      }
+      csync();
+      const double tau = tau_s[j];
+      if (tau != 0.0) {
+        const double scal = scal_s[j];
+        if (inv) {
+          const double xs = x * scal;
+#pragma unroll
+          for (int c = 0; c < IB; ++c) {
+            if (c > j) row[c] -= sbuf[c] * xs;
+            if (c == j) row[c] = xs;
+          }
+        }
+        if (MODE == GE && t == j) {
+#pragma unroll
+          for (int c = 0; c < IB; ++c)
+            if (c > j) row[c] -= sbuf[c];
+        }
+      }
+      if (MODE == GE && t == j) {
+        const double bj = beta_s[j];
+#pragma unroll
+        for (int c = 0; c < IB; ++c)
+          if (c == j) row[c] = bj;
+      }
+    }
+    csync();
+    mark(1);
+    // ---- write the block back to HBM and stage V for the trailing update
     if (MODE == GE) {
-      for (int e = tid; e < nrow * IB; e += NT) {
-        const int pr = e % nrow, j = e / nrow;
-        P[pr + j * PLD] = __ldcg(at + (rb0 + pr) + size_t(rb0 + j) * NB);
+      if (own) {
+#pragma unroll
+        for (int c = 0; c < IB; ++c) {
+          at[(rb0 + t) + size_t(rb0 + c) * NB] = row[c];
+          Vs[swz(rb0 + t, c)] = (t > c) ? row[c] : (t == c ? 1.0 : 0.0);
+        }
       }
     } else {
+      if (own) {
+#pragma unroll
+        for (int c = 0; c < IB; ++c) {
+          const bool live = (MODE == TS) || (t <= rb0 + c);
+          if (live) at[t + size_t(rb0 + c) * NB] = row[c];
+          Vs[swz(t, c)] = live ? row[c] : 0.0;
+        }
+      }
       for (int e = tid; e < IB * IB; e += NT) {
-        const int r = e % IB, j = e / IB;
-        P[r + j * PLD] = (r <= j) ? __ldcg(rt + (rb0 + r) + size_t(rb0 + j) * NB) : 0.0;
-      }
-      const int nb_rows = nrow - IB;
-      for (int e = tid; e < nb_rows * IB; e += NT) {
-        const int rr = e % nb_rows, j = e / nb_rows;
-        double v = 0.0;
-        if (MODE == TS || rr <= rb0 + j) v = __ldcg(at + rr + size_t(rb0 + j) * NB);
-        P[IB + rr + j * PLD] = v;
+        const int r = e % IB, c = e / IB;
+        if (r <= c) rt[(rb0 + r) + size_t(rb0 + c) * NB] = Ptop[e];
       }
     }
-    __syncthreads();
-    // norm^2 of column 0 over its vector rows
-    if (warp == 0) {
-      double s = 0.0;
-      for (int r = vlo(0) + lane; r < vhi(0); r += 32) s += P[r] * P[r];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) nrm2_s[0] = s;
-    }
-    // ---- level-2 Householder sweep over the ib columns (dgeqr2 / dtpqrt2)
-    for (int j = 0; j < IB; ++j) {
-      __syncthreads();
-      const double alpha = P[j + j * PLD];
-      const double xn2 = nrm2_s[j];
-      double tau = 0.0, scal = 0.0, beta = alpha;
-      if (xn2 != 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-        tau = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
-      }
-      if (tid == 0) {
-        tau_s[j] = tau;
-        scal_s[j] = scal;
-        beta_s[j] = beta;
-      }
-      const int lo = vlo(j), hi = vhi(j);
-      const double* vj = P + j * PLD;
-      // columns c = j+1.. handled by warp (c % NW)
-      int c = j + 1 + ((warp - (j + 1)) % NW + NW) % NW;
-      for (; c < IB; c += NW) {
-        double* pc = P + c * PLD;
-        if (tau != 0.0) {
-          double d = 0.0;
-          for (int r = lo + lane; r < hi; r += 32) d += vj[r] * pc[r];
-#pragma unroll
-          for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-          const double s = tau * (pc[j] + scal * d);
-          const double sv = s * scal;
-          for (int r = lo + lane; r < hi; r += 32) pc[r] -= sv * vj[r];
-          __syncwarp();
-          if (lane == 0) pc[j] -= s;
-        }
-        if (c == j + 1) {
-          __syncwarp();
-          double s2 = 0.0;
-          for (int r = vlo(c) + lane; r < vhi(c); r += 32) s2 += pc[r] * pc[r];
-#pragma unroll
-          for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-          if (lane == 0) nrm2_s[c] = s2;
-        }
-      }
-    }
-    __syncthreads();
-    // scale the reflectors, put beta on the diagonal
-    for (int e = tid; e < nrow * IB; e += NT) {
-      const int pr = e % nrow, j = e / nrow;
-      if (pr >= vlo(j) && pr < vhi(j) && tau_s[j] != 0.0) P[pr + j * PLD] *= scal_s[j];
-      if (pr == j) P[pr + j * PLD] = beta_s[j];
-    }
-    __syncthreads();
-    // ---- Gram matrix of the block's reflectors: G[i][j] = v_i . v_j (i < j)
-    for (int pidx = warp; pidx < IB * IB; pidx += NW) {
-      const int i = pidx % IB, j = pidx / IB;
-      if (i >= j) continue;
-      const double* vi = P + i * PLD;
-      const double* vjj = P + j * PLD;
-      double d = 0.0;
-      const int lo = vlo(j), hi = (MODE == TT) ? vhi(i) : vhi(j);
-      for (int r = lo + lane; r < hi; r += 32) d += vi[r] * vjj[r];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-      if (lane == 0) G[i + j * IB] = d + (MODE == GE ? vi[j] : 0.0);
-    }
-    __syncthreads();
+    csync();
+    mark(2);
     // ---- T_b by the dlarft recurrence: lane i owns row i of T
     if (warp == 0) {
       const int i = lane;
       double trow[IB];
 #pragma unroll
-      for (int j = 0; j < IB; ++j) trow[j] = 0.0;
-#pragma unroll
+      for (int l = 0; l < IB; ++l) trow[l] = 0.0;
+#pragma unroll 1
       for (int j = 0; j < IB; ++j) {
         const double tj = tau_s[j];
-        if (i == j) trow[j] = tj;
-        if (i < j) {
-          double s = 0.0;
+        double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int l = 0; l < IB; ++l)
-            if (l >= i && l < j) s += trow[l] * G[l + j * IB];
-          trow[j] = -tj * s;
-        }
+        for (int l = 0; l < IB; ++l)
+          if (l >= i && l < j) s4[l & 3] += trow[l] * G[l + j * IB];
+        const double v = (i == j) ? tj : (i < j ? -tj * ((s4[0] + s4[1]) + (s4[2] + s4[3])) : 0.0);
+#pragma unroll
+        for (int l = 0; l < IB; ++l)
+          if (l == j) trow[l] = v;
       }
 #pragma unroll
       for (int j = 0; j < IB; ++j) {
@@ -228,31 +307,8 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
         tslot[i + size_t(rb0 + j) * IB] = trow[j];
       }
     }
-    // ---- stage V for the trailing update, write the block back to HBM
-    const int vrows0 = (MODE == GE) ? rb0 : 0;
-    const int vrows1 = (MODE == GE) ? NB : (MODE == TT ? rb0 + IB : NB);
-    for (int e = tid; e < (vrows1 - vrows0) * IB; e += NT) {
-      const int rr = vrows0 + e % (vrows1 - vrows0), j = e / (vrows1 - vrows0);
-      const int col = rb0 + j;
-      double v;
-      if (MODE == GE) {
-        const int pr = rr - rb0;
-        v = (pr > j) ? P[pr + j * PLD] : (pr == j ? 1.0 : 0.0);
-        at[rr + size_t(col) * NB] = P[pr + j * PLD];
-      } else {
-        const bool live = (MODE == TS) || (rr <= col);
-        v = live ? P[IB + rr + j * PLD] : 0.0;
-        if (live) at[rr + size_t(col) * NB] = v;
-      }
-      Vs[swz(rr, j)] = v;
-    }
-    if (MODE != GE) {
-      for (int e = tid; e < IB * IB; e += NT) {
-        const int r = e % IB, j = e / IB;
-        if (r <= j) rt[(rb0 + r) + size_t(rb0 + j) * NB] = P[r + j * PLD];
-      }
-    }
-    __syncthreads();
+    csync();
+    mark(3);
     // ---- trailing update of columns rb0+IB .. NB on DMMA, 8 columns per warp
     const int nch = (NB - rb0 - IB) / 8;
     const int g0 = (MODE == GE) ? rb0 / 8 : 0;
@@ -262,10 +318,11 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
       double x[NB / 8][2];
       load_x<NB>(x, at + size_t(col) * NB, g0, g1, lane);
       double* top = (MODE == GE) ? nullptr : rt + size_t(col) * NB + rb0;
-      warp_apply<NB, true>(x, g0, g1, Vs, Ts, top, lane);
+      warp_apply<NB, true, TS>(x, g0 / (IB / 8), g1 / (IB / 8), Vs, Ts, top, lane);
       store_x<NB>(x, at + size_t(col) * NB, g0, g1, lane);
     }
-    __syncthreads();
+    csync();
+    mark(4);
   }
 }
 

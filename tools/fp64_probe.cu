@@ -53,6 +53,29 @@ __global__ void k_layout(const double* A, const double* B, double* C) {
   C[(l >> 2) * 8 + 2 * (l & 3) + 1] = c1;
 }
 
+__global__ void k_lat(double* out, long long* cyc, int n) {
+  double c0 = 0, c1 = 0;
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) dmma(c0, c1, a, b);
+  long long t1 = clock64();
+  if (threadIdx.x == 0) { cyc[0] = t1 - t0; out[1] = c0 + c1; }
+}
+// one warp per SMSP, k chains: cycles per DMMA issue
+template <int CH>
+__global__ void k_thr(double* out, long long* cyc, int n) {
+  double c[CH][2];
+  for (int i = 0; i < CH; ++i) c[i][0] = c[i][1] = 0;
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i)
+#pragma unroll
+    for (int k = 0; k < CH; ++k) dmma(c[k][0], c[k][1], a, b);
+  long long t1 = clock64();
+  double s = 0; for (int i = 0; i < CH; ++i) s += c[i][0];
+  if (threadIdx.x == 0) { cyc[0] = t1 - t0; out[2] = s; }
+}
+
 int main(int argc, char** argv) {
   double* d; cudaMalloc(&d, 1024 * sizeof(double));
   // layout check
@@ -106,6 +129,19 @@ int main(int argc, char** argv) {
     double fl = 2.0 * 32 * 8 * (double)iters * blocks * wpb;
     double t = timeit([&] { k_dfma<8><<<blocks, 32 * wpb>>>(d, iters, 1.0000001, 1e-7); }, fl);
     printf(", \"dfma_w%d_tf\": %.2f", wpb, t);
+  }
+  {
+    long long* dc; cudaMalloc(&dc, 64); long long hc;
+    k_lat<<<1, 32>>>(d, dc, 4096); cudaMemcpy(&hc, dc, 8, cudaMemcpyDeviceToHost);
+    printf(", \"dmma_latency_cyc\": %.1f", hc / 4096.0);
+    k_thr<2><<<1, 32>>>(d, dc, 2048); cudaMemcpy(&hc, dc, 8, cudaMemcpyDeviceToHost);
+    printf(", \"dmma_cyc_per_issue_2ch\": %.2f", hc / 4096.0);
+    k_thr<4><<<1, 32>>>(d, dc, 1024); cudaMemcpy(&hc, dc, 8, cudaMemcpyDeviceToHost);
+    printf(", \"dmma_cyc_per_issue_4ch\": %.2f", hc / 4096.0);
+    k_thr<8><<<1, 32>>>(d, dc, 512); cudaMemcpy(&hc, dc, 8, cudaMemcpyDeviceToHost);
+    printf(", \"dmma_cyc_per_issue_8ch\": %.2f", hc / 4096.0);
+    k_thr<8><<<1, 64>>>(d, dc, 512); cudaMemcpy(&hc, dc, 8, cudaMemcpyDeviceToHost);
+    printf(", \"dmma_cyc_per_issue_8ch_2warps\": %.2f", hc / 4096.0);
   }
   cudaError_t err = cudaDeviceSynchronize();
   printf(", \"err\": \"%s\"}\n", cudaGetErrorString(err));

@@ -49,17 +49,15 @@ def make_matrix(cfg, rows=None, row0=0):
         U = np.linalg.qr(rng.standard_normal((m, n)))[0]
         V = np.linalg.qr(rng.standard_normal((n, n)))[0]
         return np.ascontiguousarray((U * np.geomspace(1.0, 1e-12, n)) @ V.T)
-    # uniform: generate in row chunks from one stream, keep [row0, row0+rows)
+    # uniform: row chunk c (65536 rows) drawn from default_rng([seed, c]), so
+    # any block of rows is generated without the rows before it
     rows = m if rows is None else rows
     out = np.empty((rows, n))
     chunk = 65536
-    for r in range(0, m, chunk):
-        blk = rng.uniform(-1.0, 1.0, (min(chunk, m - r), n))
-        lo, hi = max(r, row0), min(r + blk.shape[0], row0 + rows)
-        if lo < hi:
-            out[lo - row0:hi - row0] = blk[lo - r:hi - r]
-        if r + chunk >= row0 + rows:
-            break
+    for c in range(row0 // chunk, (row0 + rows + chunk - 1) // chunk):
+        lo, hi = max(c * chunk, row0), min((c + 1) * chunk, row0 + rows, m)
+        blk = np.random.default_rng([cfg["seed"], c]).uniform(-1.0, 1.0, (min(chunk, m - c * chunk), n))
+        out[lo - row0:hi - row0] = blk[lo - c * chunk:hi - c * chunk]
     return out
 
 
@@ -116,7 +114,7 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def cpu_replay_rate(cfg, A, budget_flops=1.2e11, time_cap=25.0):
+def cpu_replay_rate(cfg, A, budget_flops=6e11, time_cap=25.0):
     """GFLOP/s of the LAPACK replay (oracle) on a bounded prefix of the
     workload's own trace; returns (gflops, sample description, threads)."""
     import paper_1303_3182_b200 as P
@@ -172,7 +170,7 @@ def run_reference(args, cfg):
         cfg = dict(cfg, m=A.shape[0])
     rates, desc, thr = [], "", 1
     for s in range(args.warmup + args.steps):
-        r, desc, thr = cpu_replay_rate(cfg, A, budget_flops=4e10, time_cap=8.0)
+        r, desc, thr = cpu_replay_rate(cfg, A, budget_flops=1.2e11, time_cap=10.0)
         if s >= args.warmup:
             rates.append(r)
     v = statistics.median(rates)

@@ -84,6 +84,11 @@ int tqr_build_get_updates(const tqr_build* b, int64_t* out4);
 /* build_from_trace edges (taskgraph.py:262-322): (u, v, cause) with cause
  * 0 RAW, 1 WAR, 2 WAW.  Call with uvc=NULL to get *n_out.                   */
 int tqr_build_hazard_edges(tqr_build* b, int32_t* uvc, int64_t cap, int64_t* n_out);
+/* A build holding an explicit kernel trace (kinds + 1-based indices as in
+ * tqr_build_get_trace), e.g. the cross-shard R merge of the tall-skinny
+ * path; only the trace is meaningful (no ASAP times).  Feed to
+ * tqr_plan_create like any build.                                          */
+int tqr_trace_build(int p, int q, const int8_t* kind, const int32_t* idx4, int64_t n, tqr_build** out);
 void tqr_build_free(tqr_build* b);
 
 /* ---------------- numeric engine (CUDA, sm_100a) ------------------------- */

@@ -59,6 +59,7 @@ SIGNATURES = {
     "tqr_build_get_trace": (C.c_int, [vp, i8p, i32p, i64p]),
     "tqr_build_get_updates": (C.c_int, [vp, i64p]),
     "tqr_build_hazard_edges": (C.c_int, [vp, i32p, C.c_int64, i64p]),
+    "tqr_trace_build": (C.c_int, [C.c_int, C.c_int, i8p, i32p, C.c_int64, C.POINTER(vp)]),
     "tqr_build_free": (None, [vp]),
     "tqr_plan_create": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(vp)]),
     "tqr_plan_get_info": (C.c_int, [vp, C.POINTER(PlanInfo)]),

@@ -181,6 +181,30 @@ int tqr_build_hazard_edges(tqr_build* h, int32_t* uvc, int64_t cap, int64_t* n_o
   });
 }
 
+int tqr_trace_build(int p, int q, const int8_t* kind, const int32_t* idx4, int64_t n, tqr_build** out) {
+  return tqr::guard([&] {
+    if (!(p >= 1 && q >= 1)) throw tqr::ValueError("need p >= 1 and q >= 1");
+    auto* h = new tqr_build;
+    try {
+      h->b = new tqr::Build(std::max(p, q), q, false, nullptr, true, false);
+      h->b->p = p;
+      for (int64_t t = 0; t < n; ++t) {
+        const int8_t k = kind[t];
+        if (k < 0 || k > 5) throw tqr::ValueError("bad kernel kind in trace");
+        const int32_t* x = idx4 + 4 * t;
+        const int hi_row = (k == tqr::GEQRT || k == tqr::UNMQR) ? x[0] : std::max(x[0], x[1]);
+        if (x[0] < 1 || hi_row > p) throw tqr::ValueError("trace row index out of range");
+        h->b->trace.push_back({k, x[0], x[1], x[2], x[3], 0});
+        h->b->counts[k] += 1;
+      }
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
 void tqr_build_free(tqr_build* h) { delete h; }
 
 }  // extern "C"

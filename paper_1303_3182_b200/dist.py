@@ -1,0 +1,268 @@
+"""Tall-skinny tiled QR across GPUs (BASELINE config 5).
+
+Block-row partition: rank r owns tile rows [r*P+1, (r+1)*P] of a p x q tile
+matrix (P = p/G).  Each rank factors its shard with the reference's Greedy
+tree (coarse_schedule, qr.py:254-297) — no communication.  Then log2(G)
+rounds of binary TT merges: in round s (stride 2^s) rank b = a + stride
+sends its q x q-tile R factor to rank a (one NCCL point-to-point message of
+q*q tiles), and rank a eliminates the stacked [R_a; R_b] column by column
+with TTQRT / TTMQR / GEQRT / UNMQR, pairing rows exactly as Greedy and
+Fibonacci pair them (bottom z live rows against the z rows above,
+qr.py:208-218).  Written as one global elimination list, local trees plus
+merges form a valid list under the reference's validate() (qr.py:56-83)
+with unchanged total weight (tests/test_dist.py).
+
+The numerics go through the same engine as the single-GPU path; the
+exchange is torch.distributed (NCCL on GPUs).  `Backend` isolates the
+device work so the control flow is testable with gloo on CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import statistics
+import time
+
+import numpy as np
+
+from . import _lib
+from .qr import ElimEntry, EliminationList, coarse_schedule
+from .taskgraph import GEQRT, QR_KINDS, TTMQR, TTQRT, UNMQR
+
+KIND_ID = {k: n for n, k in enumerate(QR_KINDS)}
+
+
+# ---------------------------------------------------------------------------
+# schedule side (host, exact)
+
+def merge_pairs(q, row_a, rows_b):
+    """Eliminations merging R_a (rows row_a(k)) with R_b (rows rows_b(i)):
+    per column k the live rows are [row_a(k)] + [rows_b(i) for i <= k];
+    while more than one is live, the bottom z = len//2 are zeroed by the z
+    rows directly above them."""
+    out = []
+    for k in range(1, q + 1):
+        live = [row_a(k)] + [rows_b(i) for i in range(1, k + 1)]
+        while len(live) > 1:
+            z = len(live) // 2
+            tg, pv = live[len(live) - z:], live[len(live) - 2 * z:len(live) - z]
+            for t, v in zip(tg, pv):
+                out.append(ElimEntry(t, v, k))
+            live = live[:len(live) - z]
+    return out
+
+
+def composite_list(p, q, G):
+    """Global elimination list of G local Greedy trees + binary merges."""
+    if p % G:
+        raise ValueError("p must be a multiple of the number of shards")
+    P = p // G
+    if P < q:
+        raise ValueError("each shard needs at least q tile rows")
+    _, local = coarse_schedule(P, q, "greedy")
+    entries = []
+    for s in range(G):
+        entries += [ElimEntry(e.i + s * P, e.piv + s * P, e.k) for e in local]
+    stride = 1
+    while stride < G:
+        for a in range(0, G, 2 * stride):
+            b = a + stride
+            if b < G:
+                entries += merge_pairs(q, lambda k, a=a: a * P + k, lambda i, b=b: b * P + i)
+        stride *= 2
+    return EliminationList(p, q, entries).with_steps()
+
+
+def merge_trace(q):
+    """Kernel trace of one merge on the stacked 2q x q tile matrix
+    [R_a; R_b] (rows 1..q = R_a, q+1..2q = R_b): the TT bundle of each merge
+    elimination (qr.py:494-502) — TTQRT, TTMQR for j > k, and the eliminated
+    row re-triangularized in column k+1 (GEQRT + UNMQR).  Tiles below the
+    block diagonal are structurally zero and never touched."""
+    kinds, idx = [], []
+    for e in merge_pairs(q, lambda k: k, lambda i: q + i):
+        kinds.append(KIND_ID[TTQRT])
+        idx.append((e.i, e.piv, e.k, -1))
+        for j in range(e.k + 1, q + 1):
+            kinds.append(KIND_ID[TTMQR])
+            idx.append((e.i, e.piv, e.k, j))
+        if e.k + 1 <= q:
+            kinds.append(KIND_ID[GEQRT])
+            idx.append((e.i, e.k + 1, -1, -1))
+            for j in range(e.k + 2, q + 1):
+                kinds.append(KIND_ID[UNMQR])
+                idx.append((e.i, e.k + 1, j, -1))
+    return np.asarray(kinds, dtype=np.int8), np.asarray(idx, dtype=np.int32).reshape(-1, 4)
+
+
+def emulate(A, G, nb, backend_cls=None, device=None):
+    """Single-device emulation of tall_skinny_qr with G shards (same local
+    trees and merge order; the exchange is a device copy).  For tests."""
+    p, q = A.shape[0] // nb, A.shape[1] // nb
+    P = p // G
+    be = (backend_cls or GpuBackend)(P, q, nb, device)
+    rs = []
+    for s in range(G):
+        rs.append(be.factor_local(A[s * P * nb:(s + 1) * P * nb]).clone())
+    for stride, pairs in merge_rounds(G):
+        for a, b in pairs:
+            rs[a] = be.merge(rs[a], rs[b]).clone()
+    return be, rs[0]
+
+
+def merge_rounds(G):
+    """[(stride, [(a, b), ...]), ...] — who sends (b) to whom (a)."""
+    out, stride = [], 1
+    while stride < G:
+        out.append((stride, [(a, a + stride) for a in range(0, G, 2 * stride) if a + stride < G]))
+        stride *= 2
+    return out
+
+
+# ---------------------------------------------------------------------------
+# device side
+
+class GpuBackend:
+    """Local factorization and merges with the libtqr engine."""
+
+    def __init__(self, P, q, nb, device):
+        import torch
+
+        from .engine import Plan
+        from .qr import QrBuild, build_tree
+
+        self.torch = torch
+        self.P, self.q, self.nb, self.dev = P, q, nb, device
+        self.local_plan = Plan(build_tree(P, q, "greedy"), nb)
+        kinds, idx = merge_trace(q)
+        h = C.c_void_p()
+        _lib.check(_lib.lib().tqr_trace_build(2 * q, q, kinds.ctypes.data_as(_lib.i8p), _lib.ptr_i32(idx),
+                                              len(kinds), C.byref(h)))
+        mb = QrBuild.__new__(QrBuild)
+        mb.__dict__.update(p=2 * q, q=q, family="TT", keep_trace=True, _h=h, record_updates=False)
+        self._merge_build = mb
+        self.merge_plan = Plan(mb, nb)
+        self.tiles, self.tg, self.te = self.local_plan.alloc(device)
+        self.mtiles, self.mtg, self.mte = self.merge_plan.alloc(device)
+        t2 = nb * nb
+        self.rbuf = torch.empty(q * q * t2, dtype=torch.float64, device=device)
+
+    def factor_local(self, A_local):
+        self.local_plan.pack(A_local, self.tiles)
+        self.local_plan.factor(self.tiles, self.tg, self.te)
+        # R tile rows 1..q of every tile column -> (q cols) x (q tiles)
+        t2 = self.nb * self.nb
+        src = self.tiles.view(self.q, self.P * t2)[:, :self.q * t2]
+        self.rbuf.view(self.q, self.q * t2).copy_(src)
+        return self.rbuf
+
+    def merge(self, r_a, r_b):
+        """[R_a; R_b] -> merged R (q x q tiles, written into r_a)."""
+        t2 = self.nb * self.nb
+        m = self.mtiles.view(self.q, 2 * self.q * t2)
+        m[:, :self.q * t2].copy_(r_a.view(self.q, self.q * t2))
+        m[:, self.q * t2:].copy_(r_b.view(self.q, self.q * t2))
+        self.merge_plan.factor(self.mtiles, self.mtg, self.mte)
+        r_a.view(self.q, self.q * t2).copy_(m[:, :self.q * t2])
+        return r_a
+
+    def r_matrix(self, rbuf):
+        """Upper-triangular n x n R from a q x q tile block."""
+        R = self.torch.empty((self.q * self.nb, self.q * self.nb), dtype=self.torch.float64, device=self.dev)
+        _lib.check(_lib.lib().tqr_extract_r(C.c_void_p(rbuf.data_ptr()), self.q, self.q, self.nb,
+                                            C.c_void_p(R.data_ptr()), R.shape[1], 1,
+                                            C.c_void_p(self.torch.cuda.current_stream().cuda_stream)))
+        return R
+
+
+def tall_skinny_qr(A_local, backend, rank, world, dist=None):
+    """Factor the block rows A_local on every rank; rank 0 returns the final
+    q x q-tile R block (others return None).  `dist` is torch.distributed
+    (send/recv of the R block; NCCL on GPUs, gloo in the CPU tests)."""
+    r = backend.factor_local(A_local)
+    recv = None
+    for stride, pairs in merge_rounds(world):
+        for a, b in pairs:
+            if rank == b:
+                dist.send(r, dst=a)
+            elif rank == a:
+                if recv is None:
+                    recv = r.new_empty(r.shape)
+                dist.recv(recv, src=b)
+                r = backend.merge(r, recv)
+    return r if rank == 0 else None
+
+
+# ---------------------------------------------------------------------------
+# benchmark (bench.py --gpus N, or --config c5 on one GPU)
+
+def bench_main(args, cfg, make_matrix, Clocks, cpu_replay_rate):
+    import torch
+    import torch.distributed as td
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        td.init_process_group("nccl", device_id=dev)
+    nb, m, n = cfg["nb"], cfg["m"], cfg["n"]
+    p, q = m // nb, n // nb
+    if p % world:
+        raise SystemExit(f"p={p} not divisible by world={world}")
+    P = p // world
+    rows = P * nb
+    A_host = make_matrix(cfg, rows=rows, row0=rank * rows)
+    A = torch.from_numpy(A_host).to(dev)
+    be = GpuBackend(P, q, nb, dev)
+    flops = 2.0 * n * n * (m - n / 3.0)
+
+    def step():
+        return tall_skinny_qr(A, be, rank, world, td if world > 1 else None)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        td.barrier()
+    clk = Clocks(local).start() if rank == 0 else None
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record()
+    for _ in range(args.steps):
+        out = step()
+    end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        td.barrier()
+    ms = start.elapsed_time(end) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        td.all_reduce(t, op=td.ReduceOp.MAX)
+    ms = float(t.item())
+    clocks = clk.stop() if clk else None
+    if rank == 0:
+        R = be.r_matrix(out)
+        ok = bool(torch.isfinite(R).all().item())
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            sub = dict(cfg, m=min(m, 1024 * nb))
+            rate, desc, thr = cpu_replay_rate(sub, A_host[:sub["m"]])
+            cpu = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": thr, "kind": "port", "sample": desc}
+        print(json.dumps({
+            "metric": "tiled QR fp64 GFLOP/s (2n^2(m-n/3))", "value": round(flops / (ms * 1e-3) / 1e9, 2),
+            "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c5", "m": m, "n": n, "nb": nb, "ib": 32, "tree": "greedy local + binary TT merge",
+                       "seed": cfg["seed"], "dist": "uniform(-1,1), row chunk c from default_rng([seed, c])",
+                       "parallelism": f"block rows over {world} GPU(s), NCCL p2p R merges",
+                       "l2": "inputs > 126 MB L2 (no flush needed)"},
+            "gpu_launches": (2 + 3 * (world - 1)) * args.steps,
+            "clocks": clocks, "cpu_baseline": cpu, "e2e": None,
+            "check": {"r_finite": ok},
+        }))
+    if world > 1:
+        td.destroy_process_group()

@@ -230,6 +230,46 @@ def main():
         cfg[name] = r
     g["configs"] = cfg
 
+    # 8b. tall-skinny composite lists (local Greedy per shard + binary TT
+    #     merges) through the reference's validate() and
+    #     tiled_build(): validity, CP, total weight, trace digest
+    def merge_pairs(q, row_a, rows_b):
+        out = []
+        for k in range(1, q + 1):
+            live = [row_a(k)] + [rows_b(i) for i in range(1, k + 1)]
+            while len(live) > 1:
+                z = len(live) // 2
+                for t, v in zip(live[len(live) - z:], live[len(live) - 2 * z:len(live) - z]):
+                    out.append(T.ElimEntry(t, v, k))
+                live = live[:len(live) - z]
+        return out
+
+    comp = {}
+    for p, q, G in ((64, 8, 8), (16, 4, 2), (16, 4, 4), (8192, 8, 1), (8192, 8, 2), (8192, 8, 8)):
+        P = p // G
+        _, local = T.coarse_schedule(P, q, "greedy")
+        ents = []
+        for s in range(G):
+            ents += [T.ElimEntry(e.i + s * P, e.piv + s * P, e.k) for e in local]
+        stride = 1
+        while stride < G:
+            for a in range(0, G, 2 * stride):
+                b = a + stride
+                if b < G:
+                    ents += merge_pairs(q, lambda k, a=a: a * P + k, lambda i, b=b: b * P + i)
+            stride *= 2
+        lst = T.EliminationList(p, q, ents).with_steps()
+        lst.validate()
+        b = T.tiled_build(lst, keep_trace=(p <= 64))
+        h = hashlib.sha256()
+        for e in lst:
+            h.update(f"{e.k},{e.i},{e.piv},{e.step};".encode())
+        rec = {"cp": b.cp, "total_weight": b.total_weight, "elim_sha": h.hexdigest(), "nelim": len(lst)}
+        if b.trace is not None:
+            rec["trace_sha"] = trace_digest(b.trace)
+        comp[f"{p}/{q}/{G}"] = rec
+    g["composite"] = comp
+
     # 9. CLI outputs (cli.py:112-150)
     import contextlib
     import io

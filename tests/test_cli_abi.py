@@ -1,0 +1,64 @@
+"""CLI parity with the reference's QR subcommands (golden outputs captured
+from the reference CLI) and the C ABI surface of libtqr.so."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_1303_3182_b200 import _lib
+from paper_1303_3182_b200.cli import main
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("argv", [
+    "qr-coarse --p 15 --q 6 --algo greedy --check",
+    "qr-coarse --p 9 --q 4 --algo fibonacci",
+    "qr-tiled --p 15 --q 6 --algo greedy --check",
+    "qr-tiled --p 15 --q 6 --algo plasmatree --bs 5",
+    "qr-tiled --p 10 --q 4 --algo grasap",
+    "qr-tiled --p 8 --q 4 --algo flattree --family TS",
+    "qr-coarse --p 3 --q 5",
+])
+def test_cli_matches_reference(golden, capsys, argv):
+    rec = golden["cli"][argv]
+    rc = main(argv.split())
+    cap = capsys.readouterr()
+    assert rc == rec["rc"]
+    assert cap.out == rec["out"]
+    assert cap.err == rec["err"]
+
+
+def test_cli_flags_and_outdir(tmp_path, monkeypatch, capsys):
+    assert main(["qr-tiled", "--p", "15"]) == 2
+    assert main(["nonsense"]) == 2
+    monkeypatch.setenv("TILEDAG_OUTDIR", str(tmp_path))
+    assert main(["qr-coarse", "--p", "6", "--q", "3", "--list", "--out", "t"]) == 0
+    assert (tmp_path / "t").read_text().startswith("i\\k,1,2,3")
+    assert (tmp_path / "t.elim").read_text().startswith("k,i,piv,step")
+    capsys.readouterr()
+    _, o1 = main(["qr-tiled", "--p", "10", "--q", "4", "--algo", "grasap"]), capsys.readouterr().out
+    _, o2 = main(["qr-tiled", "--p", "10", "--q", "4", "--algo", "grasap"]), capsys.readouterr().out
+    assert o1 == o2
+
+
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "tqr.h")).read()
+    decl = set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(tqr_\w+)\s*\(", hdr, re.M))
+    assert len(decl) >= 25
+    L = C.CDLL(_lib.LIB_PATH)
+    missing = [s for s in sorted(decl) if not hasattr(L, s)]
+    assert not missing, missing
+    assert set(decl) == set(_lib.SIGNATURES), set(decl) ^ set(_lib.SIGNATURES)
+    assert _lib.lib().tqr_abi_version() == 1
+
+
+def test_error_status_mapping():
+    lib = _lib.lib()
+    n = C.c_int64()
+    x = C.c_int32()
+    rc = lib.tqr_coarse_schedule(3, 5, b"greedy", None, None, 0, C.byref(n), C.byref(x))
+    assert rc == _lib.TQR_EVALUE and lib.tqr_last_error() == b"need p >= q >= 1"
+    with pytest.raises(ValueError, match="unknown coarse algorithm 'bogus'"):
+        _lib.check(lib.tqr_coarse_schedule(4, 3, b"bogus", None, None, 0, C.byref(n), C.byref(x)))

@@ -1,0 +1,138 @@
+"""Tall-skinny multi-GPU path: schedule facts on CPU, the
+NCCL exchange pattern exercised with gloo (world_size 2) and the LAPACK
+replay oracle standing in for the device kernels, and (GPU) the device
+merges emulated on one GPU."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1303_3182_b200 as P
+from paper_1303_3182_b200 import dist
+from oracle.replay import Replay, replay_build, row_sign_normalize
+
+from _digest import build_digest, elim_sha
+
+
+@pytest.mark.parametrize("key", ["64/8/8", "16/4/2", "16/4/4", "8192/8/1", "8192/8/2", "8192/8/8"])
+def test_composite_list_matches_reference(golden, key):
+    p, q, G = (int(x) for x in key.split("/"))
+    rec = golden["composite"][key]
+    lst = dist.composite_list(p, q, G)
+    assert lst.validate()
+    assert len(lst) == rec["nelim"] and elim_sha(lst) == rec["elim_sha"]
+    b = P.tiled_build(lst, keep_trace=(p <= 64))
+    assert b.cp == rec["cp"] and b.total_weight == rec["total_weight"] == P.total_weight(p, q)
+    if "trace_sha" in rec:
+        assert build_digest(b) == rec["trace_sha"]
+
+
+def test_merge_trace_is_the_tail_of_the_global_trace():
+    p, q, G = 16, 4, 2
+    Pp = p // G
+    b = P.tiled_build(dist.composite_list(p, q, G))
+    kinds, idx, _ = b.trace_arrays()
+    mk, mi = dist.merge_trace(q)
+    tail_k, tail_i = kinds[-len(mk):], idx[-len(mk):]
+    assert (tail_k == mk).all()
+
+    def to_local(r):  # global row -> merge-matrix row
+        if r <= 0:
+            return r
+        return r if r <= Pp else q + (r - Pp)
+    arity = (2, 3, 3, 3, 4, 4)
+    for kd, g, l in zip(tail_k, tail_i, mi):
+        n_rows = 1 if kd in (0, 3) else 2
+        exp = [to_local(int(x)) if t < n_rows else int(x) for t, x in enumerate(g[:arity[kd]])]
+        assert exp == [int(x) for x in l[:arity[kd]]]
+
+
+class CpuOracleBackend:
+    """LAPACK-replay stand-in for GpuBackend (test infrastructure only)."""
+
+    def __init__(self, Pp, q, nb, device=None):
+        self.Pp, self.q, self.nb = Pp, q, nb
+        self.kinds, self.idx = dist.merge_trace(q)
+
+    def _block(self, tiles):
+        out = torch.empty(self.q * self.q * self.nb * self.nb, dtype=torch.float64)
+        v = out.view(self.q, self.q, self.nb * self.nb)
+        for j in range(self.q):
+            for i in range(self.q):
+                v[j, i] = torch.from_numpy(np.ascontiguousarray(tiles[i][j].reshape(-1, order="F")))
+        return out
+
+    def _tiles(self, blk):
+        v = blk.view(self.q, self.q, self.nb * self.nb).numpy()
+        return [[np.asfortranarray(v[j, i].reshape(self.nb, self.nb, order="F")) for j in range(self.q)]
+                for i in range(self.q)]
+
+    def factor_local(self, A_local):
+        b = P.build_tree(self.Pp, self.q, "greedy")
+        rp = replay_build(A_local.numpy(), b, self.nb)
+        return self._block(rp.t)
+
+    def merge(self, r_a, r_b):
+        rp = Replay.__new__(Replay)
+        rp.p, rp.q, rp.nb, rp.ib = 2 * self.q, self.q, self.nb, 32
+        rp.t = self._tiles(r_a) + self._tiles(r_b)
+        rp.tg, rp.te = {}, {}
+        rp.run(self.kinds, self.idx)
+        return self._block(rp.t[:self.q])
+
+
+def _full_r(blk, q, nb):
+    v = blk.view(q, q, nb * nb).numpy()
+    R = np.zeros((q * nb, q * nb))
+    for j in range(q):
+        for i in range(j + 1):
+            R[i * nb:(i + 1) * nb, j * nb:(j + 1) * nb] = v[j, i].reshape(nb, nb, order="F")
+    return np.triu(R)
+
+
+def _matrix(p, q, nb, seed=4):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, (p * nb, q * nb))
+
+
+def _worker(rank, world, port, p, q, nb, out):
+    import torch.distributed as td
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    A = _matrix(p, q, nb)
+    Pp = p // world
+    A_local = torch.from_numpy(A[rank * Pp * nb:(rank + 1) * Pp * nb].copy())
+    r = dist.tall_skinny_qr(A_local, CpuOracleBackend(Pp, q, nb), rank, world, td)
+    if rank == 0:
+        R = row_sign_normalize(_full_r(r, q, nb))
+        Rref = row_sign_normalize(np.linalg.qr(A, mode="r"))
+        out.put(float(np.linalg.norm(R - Rref) / np.linalg.norm(A)))
+    td.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_exchange_and_merge(world):
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_worker, args=(world, port, 8, 2, 64, q), nprocs=world, join=True)
+    err = q.get(timeout=60)
+    assert err <= 1e-13, err
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G,p,q,nb", [(2, 8, 2, 64), (4, 16, 4, 64), (2, 8, 4, 256)])
+def test_gpu_emulated_shards(G, p, q, nb):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    A = _matrix(p, q, nb, seed=7)
+    At = torch.from_numpy(A).cuda()
+    be, r = dist.emulate(At, G, nb, device=torch.device("cuda"))
+    R = row_sign_normalize(be.r_matrix(r).cpu().numpy())
+    Rref = row_sign_normalize(np.linalg.qr(A, mode="r"))
+    assert np.linalg.norm(R - Rref) <= 1e-11 * np.linalg.norm(A)

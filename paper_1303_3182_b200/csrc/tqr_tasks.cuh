@@ -19,9 +19,13 @@ struct Smem {
   static constexpr int TOP = IB * WS;  // staged pivot rows of a slab (TT/TS)
   static constexpr int U_V0 = 0, U_V1 = VS, U_T0 = 2 * VS, U_T1 = 2 * VS + TS, U_P0 = 2 * VS + 2 * TS,
                        U_P1 = U_P0 + TOP, U_END = U_P1 + TOP;
-  // panel layout
-  static constexpr int P_TOP = 0, P_V = TS, P_T = P_V + VS, P_G = P_T + TS, P_PART = P_G + TS;
-  static constexpr int P_DROW = P_PART + NW * IB, P_SBUF = P_DROW + IB, P_SC = P_SBUF + IB;
+  // panel layout: stacked panel P (column-major, ld PLD = 4 mod 16), staged
+  // V/T for the trailing update, Gram, T, group-update partials and scalars
+  static constexpr int PLD = NB + IB + 4;
+  static constexpr int LDW = IB + 4;
+  static constexpr int P_P = 0, P_V = P_P + PLD * IB, P_T = P_V + VS, P_G = P_T + TS, P_TT = P_G + TS;
+  static constexpr int P_WP = P_TT + TS, P_W = P_WP + NW * 8 * LDW, P_TG = P_W + 8 * LDW;
+  static constexpr int P_PART = P_TG + 64, P_DROW = P_PART + 2 * NW * 8, P_SBUF = P_DROW + 16, P_SC = P_SBUF + 8;
   static constexpr int P_END = P_SC + 3 * IB + 8;
   static constexpr int END = U_END > P_END ? U_END : P_END;
   static constexpr size_t BYTES = size_t(END) * sizeof(double);
@@ -118,40 +122,65 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
 
 // ---------------------------------------------------------------------------
 // panel item: Householder QR of one tile (GE), of [R_piv; R_i] (TT) or of
-// [R_piv; A_i] (TS), ib columns at a time.  Level-2 sweep of a block with
-// one panel row per thread held in registers: per column a single 32-wide
-// warp reduce-scatter yields the column norm, the dots with the trailing
-// columns (the reflector application) and the dots with the previous
-// reflectors (the Gram column that builds T) — two CTA barriers per column.
-// Then T_b (dlarft recurrence) and the block reflector applied to the
-// trailing columns on DMMA.
+// [R_piv; A_i] (TS), ib = 32 columns at a time, each block in four groups of
+// 8 columns.  Within a group: one panel row (or two) per thread in
+// registers, per column one 8-value warp reduce-scatter gives the norm and
+// the dots with the group's later columns (dlarfg + reflector application,
+// two CTA barriers per column).  After a group: one DMMA pass
+// V_g^T [V_g | A_rest] (K = rows split over warps) yields the group Gram
+// (-> T_g) and W; A_rest -= V_g T_g^T W on DMMA.  After the block: the
+// 32x32 Gram V^T V on DMMA, T_b by back substitution, and the block
+// reflector applied to the trailing columns of the tile(s) on DMMA.
+//
+// Stacked panel rows (P, panel-local): GE rows = tile rows rb0..NB-1 (the
+// diagonal row of column j is row j); TT/TS rows 0..IB-1 = pivot block rows
+// rb0.. (diagonal row j = row j), rows IB.. = bottom tile rows 0.. .
 
 __device__ __forceinline__ unsigned long long ptimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
+  unsigned long long tt;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tt));
+  return tt;
 }
 
-// prof (optional, diagnostics): ns accumulated per phase
-// [0 load, 1 level-2, 2 write-back/stage, 3 T, 4 trailing update] + MODE*8
+template <int NB, int MODE>
+__device__ __forceinline__ double vmask_p(double v, int row, int col) {
+  // reflector entry of P row `row`, block column `col`
+  if (MODE == GE) return row > col ? v : (row == col ? 1.0 : 0.0);
+  return row >= IB ? v : (row == col ? 1.0 : 0.0);
+}
+
+// C(8 x 8*NBK) += V(:, cv0..cv0+7)^T * [V(:, cv0..cv0+7) | P(:, cv0+8..)]
+// over rows [k0, k1) (multiple of 4), one warp; n-block 0 is the group's
+// own reflectors (masked, -> Gram), the rest raw panel columns.  Lane (r,c)
+// holds C[r][8nb + 2c + i].
+template <int NB, int MODE, int NBK>
+__device__ __forceinline__ void tn_acc(double (&acc)[NBK][2], const double* P, int cv0, int k0, int k1, int lane) {
+  constexpr int PLD = NB + IB + 4;
+  const int r = lane >> 2, c = lane & 3;
+  for (int k = k0; k < k1; k += 4) {
+    const int row = k + c;
+    const double a = vmask_p<NB, MODE>(P[row + (cv0 + r) * PLD], row, cv0 + r);
+    dmma(acc[0], a, a);  // B(k=c, n=r) = V[row][cv0+r]: the same element as this lane's A
+#pragma unroll
+    for (int nb = 1; nb < NBK; ++nb) dmma(acc[nb], a, P[row + (cv0 + 8 * nb + r) * PLD]);
+  }
+}
+
 template <int NB, int MODE>
 __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile (i,k)*/,
                            double* rt /*TT/TS: pivot tile (piv,k)*/, double* tslot, int tid,
                            unsigned long long* prof = nullptr) {
-  unsigned long long tp = (prof && tid == 0) ? ptimer() : 0;
-  auto mark = [&](int ph) {
-    if (prof && tid == 0) {
-      const unsigned long long t2 = ptimer();
-      atomicAdd(prof + MODE * 8 + ph, t2 - tp);
-      tp = t2;
-    }
-  };
   using S = Smem<NB>;
+  constexpr int PLD = S::PLD, LDW = S::LDW;
   const int warp = tid >> 5, lane = tid & 31;
-  double* Ptop = sm + S::P_TOP;  // TT/TS: top block, column-major ld IB
+  double* P = sm + S::P_P;
   double* Vs = sm + S::P_V;
   double* Ts = sm + S::P_T;
-  double* G = sm + S::P_G;  // G[i + j*IB] = v_i . v_j, i < j
+  double* G = sm + S::P_G;    // G[l + j*IB] = v_l . v_j
+  double* Tp = sm + S::P_TT;  // T_b plain, row-major Tp[i*IB + j]
+  double* WP = sm + S::P_WP;  // [warp][8][LDW] partial W
+  double* W = sm + S::P_W;    // [8][LDW]
+  double* Tg = sm + S::P_TG;  // 8x8 group T, Tg[i + j*8]
   double* part = sm + S::P_PART;
   double* drow = sm + S::P_DROW;
   double* sbuf = sm + S::P_SBUF;
@@ -159,152 +188,363 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
   double* scal_s = tau_s + IB;
   double* beta_s = tau_s + 2 * IB;
   const int t = tid;
+  unsigned long long tp = (prof && tid == 0) ? ptimer() : 0;
+  auto mark = [&](int ph) {
+    if (prof && tid == 0) {
+      const unsigned long long t2 = ptimer();
+      atomicAdd(prof + MODE * 16 + ph, t2 - tp);
+      tp = t2;
+    }
+  };
 
   for (int b = 0; b < NB / IB; ++b) {
     const int rb0 = b * IB;
-    // thread t owns panel row t: GE tile row rb0+t; TT/TS bottom-tile row t
-    const int nrows = (MODE == GE) ? NB - rb0 : (MODE == TT ? rb0 + IB : NB);
-    const bool own = t < nrows;
-    double row[IB];
-#pragma unroll
-    for (int c = 0; c < IB; ++c) {
-      double v = 0.0;
-      if (own) {
-        if (MODE == GE)
-          v = __ldcg(at + (rb0 + t) + size_t(rb0 + c) * NB);
-        else if (MODE == TS || t <= rb0 + c)
-          v = __ldcg(at + t + size_t(rb0 + c) * NB);
+    const int nrows = (MODE == GE) ? NB - rb0 : (MODE == TT ? IB + rb0 + IB : IB + NB);
+    // ---- load the stacked panel into smem
+    if (MODE == GE) {
+      for (int e = tid; e < nrows * IB; e += NT) {
+        const int r = e % nrows, c = e / nrows;
+        P[r + c * PLD] = __ldcg(at + (rb0 + r) + size_t(rb0 + c) * NB);
       }
-      row[c] = v;
-    }
-    if (MODE != GE) {
+    } else {
       for (int e = tid; e < IB * IB; e += NT) {
         const int r = e % IB, c = e / IB;
-        Ptop[e] = (r <= c) ? __ldcg(rt + (rb0 + r) + size_t(rb0 + c) * NB) : 0.0;
+        P[r + c * PLD] = (r <= c) ? __ldcg(rt + (rb0 + r) + size_t(rb0 + c) * NB) : 0.0;
+      }
+      const int nb_rows = nrows - IB;
+      for (int e = tid; e < nb_rows * IB; e += NT) {
+        const int rr = e % nb_rows, c = e / nb_rows;
+        double v = 0.0;
+        if (MODE == TS || rr <= rb0 + c) v = __ldcg(at + rr + size_t(rb0 + c) * NB);
+        P[IB + rr + c * PLD] = v;
       }
     }
     csync();
     mark(0);
-    // ---- level-2 sweep (dgeqr2 / dtpqrt2 semantics, LAPACK dlarfg).  A
-    // runtime loop (small code: the unrolled version is I-cache bound); the
-    // register row is indexed statically under predicates.
-#pragma unroll 1
-    for (int j = 0; j < IB; ++j) {
-      if (MODE == GE && t == j) {
+    // rows owned by this thread: t and t+NT
+    const int r0w = t, r1w = t + NT;
+    const bool own0 = r0w < nrows, own1 = r1w < nrows;
+    auto in_vec = [&](int r, int j) {  // P row r belongs to reflector j's vector part
+      if (MODE == GE) return r > j;
+      if (MODE == TT) return r >= IB && r <= IB + rb0 + j;
+      return r >= IB;
+    };
+    for (int gq = 0; gq < IB / 8; ++gq) {
+      const int c0 = 8 * gq;
+      // ---- level-2 on columns c0..c0+7 (registers: 8 values per owned row)
+      double rv0[8], rv1[8];
 #pragma unroll
-        for (int c = 0; c < IB; ++c) drow[c] = row[c];
+      for (int c = 0; c < 8; ++c) {
+        rv0[c] = own0 ? P[r0w + (c0 + c) * PLD] : 0.0;
+        rv1[c] = own1 ? P[r1w + (c0 + c) * PLD] : 0.0;
       }
-      const bool inv = (MODE == GE) ? (own && t > j) : (MODE == TT ? (t <= rb0 + j) : own);
-      double xj = 0.0;
 #pragma unroll
-      for (int c = 0; c < IB; ++c) xj = (c == j) ? row[c] : xj;
-      const double x = inv ? xj : 0.0;
-      double d[IB];
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = c0 + jj;
+        double* partj = part + (jj & 1) * (NW * 8);  // double-buffered by column parity
+        double* drowj = drow + (jj & 1) * 8;
+        if (t == j) {
 #pragma unroll
-      for (int c = 0; c < IB; ++c) d[c] = x * row[c];
-      part[warp * IB + lane] = warp_reduce_scatter32(d, lane);
-      csync();
-      if (warp == 0) {
+          for (int c = 0; c < 8; ++c) drowj[c] = rv0[c];
+        }
+        const bool iv0 = own0 && in_vec(r0w, j), iv1 = own1 && in_vec(r1w, j);
+        const double x0 = iv0 ? rv0[jj] : 0.0, x1 = iv1 ? rv1[jj] : 0.0;
+        double d[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) d[c] = x0 * rv0[c] + x1 * rv1[c];
+        // reduce-scatter 8 values over the warp: lane L ends with value
+        // v(L) = 4*bit4 + 2*bit3 + bit2 summed over all 32 lanes
+        {
+          const bool u4 = lane & 16;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const double snd = u4 ? d[i] : d[i + 4], kp = u4 ? d[i + 4] : d[i];
+            d[i] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+          }
+          const bool u3 = lane & 8;
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const double snd = u3 ? d[i] : d[i + 2], kp = u3 ? d[i + 2] : d[i];
+            d[i] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+          }
+          const bool u2 = lane & 4;
+          {
+            const double snd = u2 ? d[0] : d[1], kp = u2 ? d[1] : d[0];
+            d[0] = kp + __shfl_xor_sync(0xffffffffu, snd, 4);
+          }
+          d[0] += __shfl_xor_sync(0xffffffffu, d[0], 2);
+          d[0] += __shfl_xor_sync(0xffffffffu, d[0], 1);
+          if ((lane & 3) == 0) partj[warp * 8 + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = d[0];
+        }
+        csync();
+        // every warp: lane v (mod 8) sums value v over the warps and computes
+        // the reflector scalars redundantly (no second barrier)
+        const int v = lane & 7;
         double D = 0.0;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) D += part[w * IB + lane];
-        const double alpha = (MODE == GE) ? drow[j] : Ptop[j + j * IB];
-        const double xn2 = __shfl_sync(0xffffffffu, D, j);
+        for (int w = 0; w < NW; ++w) D += partj[w * 8 + v];
+        const double alpha = drowj[jj];
+        const double xn2 = __shfl_sync(0xffffffffu, D, jj);
         double tau = 0.0, scal = 0.0, beta = alpha;
         if (xn2 != 0.0) {
           beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-          const double rb = 1.0 / beta;
-          tau = (beta - alpha) * rb;
+          tau = (beta - alpha) / beta;
           scal = 1.0 / (alpha - beta);
         }
-        const double dr = (MODE == GE) ? drow[lane] : Ptop[j + lane * IB];
-        if (lane > j) {
-          const double sc = tau * (dr + scal * D);
-          sbuf[lane] = sc;
-          if (MODE != GE) Ptop[j + lane * IB] = dr - sc;
-        }
-        if (lane < j) G[lane + j * IB] = scal * D + ((MODE == GE) ? dr : 0.0);
-        if (MODE != GE && lane == j) Ptop[j + j * IB] = beta;
-        if (lane == 0) {
+        const double sv = tau * (drowj[v] + scal * D);
+        if (tid == 0) {
           tau_s[j] = tau;
           scal_s[j] = scal;
           beta_s[j] = beta;
         }
-      }
-      csync();
-      const double tau = tau_s[j];
-      if (tau != 0.0) {
-        const double scal = scal_s[j];
-        if (inv) {
-          const double xs = x * scal;
+        if (tau != 0.0) {
+          double s[8];
 #pragma unroll
-          for (int c = 0; c < IB; ++c) {
-            if (c > j) row[c] -= sbuf[c] * xs;
-            if (c == j) row[c] = xs;
+          for (int c = jj + 1; c < 8; ++c) s[c] = __shfl_sync(0xffffffffu, sv, c);
+          if (iv0) {
+            const double xs = x0 * scal;
+#pragma unroll
+            for (int c = jj + 1; c < 8; ++c) rv0[c] -= s[c] * xs;
+            rv0[jj] = xs;
+          }
+          if (iv1) {
+            const double xs = x1 * scal;
+#pragma unroll
+            for (int c = jj + 1; c < 8; ++c) rv1[c] -= s[c] * xs;
+            rv1[jj] = xs;
+          }
+          if (t == j) {
+#pragma unroll
+            for (int c = jj + 1; c < 8; ++c) rv0[c] -= s[c];
           }
         }
-        if (MODE == GE && t == j) {
-#pragma unroll
-          for (int c = 0; c < IB; ++c)
-            if (c > j) row[c] -= sbuf[c];
-        }
+        if (t == j) rv0[jj] = beta;
+        mark(7);
       }
-      if (MODE == GE && t == j) {
-        const double bj = beta_s[j];
 #pragma unroll
-        for (int c = 0; c < IB; ++c)
-          if (c == j) row[c] = bj;
+      for (int c = 0; c < 8; ++c) {
+        if (own0) P[r0w + (c0 + c) * PLD] = rv0[c];
+        if (own1) P[r1w + (c0 + c) * PLD] = rv1[c];
+      }
+      csync();
+      mark(1);
+      // ---- group update: W = V_g^T [V_g | A_rest] (DMMA, K = rows over warps)
+      if (gq < IB / 8 - 1) {
+        const int ncol = IB - c0 - 8;  // 24, 16, 8
+        // rows that can hold nonzero reflector entries of this group
+        const int klo = (MODE == GE) ? (c0 & ~3) : 0;
+        const int khi = (MODE == GE) ? nrows : (MODE == TT ? IB + rb0 + c0 + 8 : nrows);
+        const int ksteps = (khi - klo + 3) >> 2;
+        const int per = (ksteps + NW - 1) / NW;
+        const int ka = klo + 4 * per * warp, kb = min(khi, ka + 4 * per);
+        double acc[4][2];
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
+        if (ka < kb) {
+          // rows beyond nrows are read as zero: clamp to a multiple of 4 within P
+          const int kbb = ((kb - ka + 3) & ~3) + ka;
+          if (ncol == 24)
+            tn_acc<NB, MODE, 4>(acc, P, c0, ka, kbb, lane);
+          else if (ncol == 16)
+            tn_acc<NB, MODE, 3>(reinterpret_cast<double(&)[3][2]>(acc), P, c0, ka, kbb, lane);
+          else
+            tn_acc<NB, MODE, 2>(reinterpret_cast<double(&)[2][2]>(acc), P, c0, ka, kbb, lane);
+        }
+        {
+          const int r = lane >> 2, c = lane & 3;
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) {
+            WP[(warp * 8 + r) * LDW + 8 * nb + 2 * c] = acc[nb][0];
+            WP[(warp * 8 + r) * LDW + 8 * nb + 2 * c + 1] = acc[nb][1];
+          }
+        }
+        csync();
+        for (int e = tid; e < 8 * (8 + ncol); e += NT) {
+          const int jr = e / (8 + ncol), cc = e % (8 + ncol);
+          double s = 0.0;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) s += WP[(w * 8 + jr) * LDW + cc];
+          W[jr * LDW + cc] = s;
+        }
+        csync();
+        // T_g (8x8) = (diag(1/tau) + striu(G_g))^-1 by back substitution;
+        // lane cc owns column cc
+        if (warp == 0 && lane < 8) {
+          const int cc = lane;
+          double col[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) col[i] = 0.0;
+#pragma unroll
+          for (int i = 7; i >= 0; --i) {
+            double v = 0.0;
+            if (i == cc) v = tau_s[c0 + i];
+            if (i < cc) {
+              double s = 0.0;
+#pragma unroll
+              for (int l = i + 1; l < 8; ++l)
+                if (l <= cc) s += W[i * LDW + l] * col[l];
+              v = -tau_s[c0 + i] * s;
+            }
+            col[i] = v;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) Tg[i + cc * 8] = col[i];
+        }
+        csync();
+        // W_rest <- T_g^T W_rest
+        for (int e = tid; e < 8 * ncol; e += NT) {
+          const int jr = e / ncol, cc = 8 + e % ncol;
+          double s = 0.0;
+#pragma unroll
+          for (int l = 0; l < 8; ++l)
+            if (l <= jr) s += Tg[l + jr * 8] * W[l * LDW + cc];
+          WP[jr * LDW + cc] = s;  // reuse warp-0 slab of WP as the result
+        }
+        csync();
+        // A_rest -= V_g W_rest: m-blocks of 8 rows round-robin over warps
+        {
+          const int r = lane >> 2, c = lane & 3;
+          const int mlo = klo >> 3, mhi = (khi + 7) >> 3;
+          for (int mb = mlo + warp; mb < mhi; mb += NW) {
+            const int row = 8 * mb + r;
+            // A fragments: V[row][c0 + 4kk + c], k = reflector index
+            double a0 = vmask_p<NB, MODE>(P[row + (c0 + c) * PLD], row, c0 + c);
+            double a1 = vmask_p<NB, MODE>(P[row + (c0 + 4 + c) * PLD], row, c0 + 4 + c);
+            for (int nb = 0; nb < ncol / 8; ++nb) {
+              const int cb = c0 + 8 + 8 * nb;
+              double acc2[2];
+              acc2[0] = P[8 * mb + r + (cb + 2 * c) * PLD];
+              acc2[1] = P[8 * mb + r + (cb + 2 * c + 1) * PLD];
+              const double b0 = -WP[c * LDW + 8 + 8 * nb + r];
+              const double b1 = -WP[(4 + c) * LDW + 8 + 8 * nb + r];
+              dmma(acc2, a0, b0);
+              dmma(acc2, a1, b1);
+              if (row < nrows) {
+                P[8 * mb + r + (cb + 2 * c) * PLD] = acc2[0];
+                P[8 * mb + r + (cb + 2 * c + 1) * PLD] = acc2[1];
+              }
+            }
+          }
+        }
+        csync();
+        mark(2);
+      }
+    }
+    // ---- block Gram G = V^T V (32x32, upper blocks) on DMMA: warp w takes
+    // (m-block, n-block) pairs of the 4x4 block grid with m <= n
+    {
+      const int klo = 0, khi = (nrows + 3) & ~3;
+      for (int pr = warp; pr < 10; pr += NW) {
+        const int mb = pr < 4 ? 0 : (pr < 7 ? 1 : (pr < 9 ? 2 : 3));
+        const int nbb = pr < 4 ? pr : (pr < 7 ? pr - 3 : (pr < 9 ? pr - 5 : 3));
+        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // two chains (k even/odd steps)
+        const int r = lane >> 2, c = lane & 3;
+        for (int k = klo; k < khi; k += 8) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int row = k + 4 * h + c;
+            if (k + 4 * h < khi) {
+              const double a = vmask_p<NB, MODE>(P[row + (8 * mb + r) * PLD], row, 8 * mb + r);
+              const double bv = vmask_p<NB, MODE>(P[row + (8 * nbb + r) * PLD], row, 8 * nbb + r);
+              dmma(acc[h], a, bv);
+            }
+          }
+        }
+        G[(8 * mb + r) + (8 * nbb + 2 * c) * IB] = acc[0][0] + acc[1][0];
+        G[(8 * mb + r) + (8 * nbb + 2 * c + 1) * IB] = acc[0][1] + acc[1][1];
       }
     }
     csync();
-    mark(1);
-    // ---- write the block back to HBM and stage V for the trailing update
-    if (MODE == GE) {
-      if (own) {
+    mark(5);
+    // ---- T_b = U^-1, U = diag(1/tau) + striu(G) (dlarft, forward columnwise):
+    // the four 8x8 diagonal blocks by back substitution (lane = column),
+    // then two block levels T12 = -T11 G12 T22 with all threads
+    for (int e = tid; e < IB * IB; e += NT) Tp[e] = 0.0;
+    csync();
+    if (warp < 4 && lane < 8) {
+      const int g0 = warp * 8, cc = lane;
+      double col[8];
 #pragma unroll
-        for (int c = 0; c < IB; ++c) {
-          at[(rb0 + t) + size_t(rb0 + c) * NB] = row[c];
-          Vs[swz(rb0 + t, c)] = (t > c) ? row[c] : (t == c ? 1.0 : 0.0);
+      for (int i = 7; i >= 0; --i) {
+        double v = 0.0;
+        if (i == cc) v = tau_s[g0 + i];
+        if (i < cc) {
+          double s = 0.0;
+#pragma unroll
+          for (int l = i + 1; l < 8; ++l)
+            if (l <= cc) s += G[(g0 + i) + (g0 + l) * IB] * col[l];
+          v = -tau_s[g0 + i] * s;
         }
+        col[i] = v;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) Tp[(g0 + i) * IB + g0 + cc] = col[i];
+    }
+    csync();
+    double* M = WP;  // scratch, row-major IB x IB
+    // level 1: blocks (0,1) and (2,3): M = G12 T22, then T12 = -T11 M
+    if (tid < 128) {
+      const int pb = tid >> 6, e = tid & 63, i = e >> 3, jx = e & 7;
+      const int a0 = 16 * pb, b0 = a0 + 8;
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l < 8; ++l) s += G[(a0 + i) + (b0 + l) * IB] * Tp[(b0 + l) * IB + b0 + jx];
+      M[(a0 + i) * IB + b0 + jx] = s;
+    }
+    csync();
+    if (tid < 128) {
+      const int pb = tid >> 6, e = tid & 63, i = e >> 3, jx = e & 7;
+      const int a0 = 16 * pb, b0 = a0 + 8;
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l < 8; ++l) s += Tp[(a0 + i) * IB + a0 + l] * M[(a0 + l) * IB + b0 + jx];
+      Tp[(a0 + i) * IB + b0 + jx] = -s;
+    }
+    csync();
+    // level 2: rows 0..15 x cols 16..31
+    {
+      const int i = tid >> 4, jx = tid & 15;
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l < 16; ++l) s += G[i + (16 + l) * IB] * Tp[(16 + l) * IB + 16 + jx];
+      M[i * IB + 16 + jx] = s;
+    }
+    csync();
+    {
+      const int i = tid >> 4, jx = tid & 15;
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l < 16; ++l) s += Tp[i * IB + l] * M[l * IB + 16 + jx];
+      Tp[i * IB + 16 + jx] = -s;
+    }
+    csync();
+    mark(6);
+    // ---- write the block back to HBM, stage V and T for the trailing update
+    for (int e = tid; e < IB * IB; e += NT) {
+      const int i = e % IB, j = e / IB;
+      const double v = Tp[i * IB + j];
+      Ts[swz(i, j)] = v;
+      tslot[i + size_t(rb0 + j) * IB] = v;
+    }
+    if (MODE == GE) {
+      for (int e = tid; e < nrows * IB; e += NT) {
+        const int r = e % nrows, c = e / nrows;
+        const double v = P[r + c * PLD];
+        at[(rb0 + r) + size_t(rb0 + c) * NB] = v;
+        Vs[swz(rb0 + r, c)] = (r > c) ? v : (r == c ? 1.0 : 0.0);
       }
     } else {
-      if (own) {
-#pragma unroll
-        for (int c = 0; c < IB; ++c) {
-          const bool live = (MODE == TS) || (t <= rb0 + c);
-          if (live) at[t + size_t(rb0 + c) * NB] = row[c];
-          Vs[swz(t, c)] = live ? row[c] : 0.0;
-        }
-      }
       for (int e = tid; e < IB * IB; e += NT) {
         const int r = e % IB, c = e / IB;
-        if (r <= c) rt[(rb0 + r) + size_t(rb0 + c) * NB] = Ptop[e];
+        if (r <= c) rt[(rb0 + r) + size_t(rb0 + c) * NB] = P[r + c * PLD];
       }
-    }
-    csync();
-    mark(2);
-    // ---- T_b by the dlarft recurrence: lane i owns row i of T
-    if (warp == 0) {
-      const int i = lane;
-      double trow[IB];
-#pragma unroll
-      for (int l = 0; l < IB; ++l) trow[l] = 0.0;
-#pragma unroll 1
-      for (int j = 0; j < IB; ++j) {
-        const double tj = tau_s[j];
-        double s4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int l = 0; l < IB; ++l)
-          if (l >= i && l < j) s4[l & 3] += trow[l] * G[l + j * IB];
-        const double v = (i == j) ? tj : (i < j ? -tj * ((s4[0] + s4[1]) + (s4[2] + s4[3])) : 0.0);
-#pragma unroll
-        for (int l = 0; l < IB; ++l)
-          if (l == j) trow[l] = v;
-      }
-#pragma unroll
-      for (int j = 0; j < IB; ++j) {
-        Ts[swz(i, j)] = trow[j];
-        tslot[i + size_t(rb0 + j) * IB] = trow[j];
+      const int nb_rows = nrows - IB;
+      for (int e = tid; e < nb_rows * IB; e += NT) {
+        const int rr = e % nb_rows, c = e / nb_rows;
+        const bool live = (MODE == TS) || (rr <= rb0 + c);
+        const double v = live ? P[IB + rr + c * PLD] : 0.0;
+        if (live) at[rr + size_t(rb0 + c) * NB] = v;
+        Vs[swz(rr, c)] = v;
       }
     }
     csync();

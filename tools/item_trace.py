@@ -64,12 +64,12 @@ def main():
         out["per_kind"][KIND[kd]] = {"n": int(msk.sum()), "mean_us": float(dur.mean()), "p50_us": float(np.median(dur)),
                                      "p90_us": float(np.percentile(dur, 90)), "sum_ms": float(dur.sum() / 1e3),
                                      "mean_wait_us": float(wait.mean()), "sum_wait_ms": float(wait.sum() / 1e3)}
-    names = ["load", "level2", "writeback", "T", "trailing"]
+    names = ["load", "l2_tail", "group_upd", "writeback", "trailing", "gram", "T", "l2_reduce", "l2_D"]
     for md, nm in ((0, "GEQRT"), (1, "TTQRT"), (2, "TSQRT")):
         cnt = int((items[:, 0] == md).sum())
         if cnt:
-            out.setdefault("panel_phases_us", {})[nm] = {names[k]: round(float(prof[md * 8 + k]) / 1e3 / cnt, 2)
-                                                        for k in range(5)}
+            out.setdefault("panel_phases_us", {})[nm] = {names[k]: round(float(prof[md * 16 + k]) / 1e3 / cnt, 2)
+                                                        for k in range(len(names))}
     nsm = int(sm.max()) + 1
     busy = (end - rdy).sum()
     waits = (rdy - deq).sum()

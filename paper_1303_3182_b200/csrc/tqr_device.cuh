@@ -125,19 +125,16 @@ struct NoPf {
   __device__ __forceinline__ void flush() const {}
 };
 
-// MASK (GE unit-lower / TT upper-triangular / TS none) is applied to the
-// B fragments of row block `drb` (the reflector block's diagonal 32x32).
-template <int NB, bool TRANST, int MASK, class PF = NoPf>
+// TRI: shape of row block `drb` of V (the reflector block's diagonal 32x32):
+// 0 unit-lower (GE), 1 upper (TT), 2 full (TS).  V is staged already
+// masked; 8x8 sub-blocks that are structurally zero are skipped in both
+// GEMMs.
+template <int NB, bool TRANST, int TRI = 2, class PF = NoPf>
 __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int rb1, const double* __restrict__ Vs,
                                            const double* __restrict__ Ts, double* top, int lane,
                                            const double* top_s = nullptr, int drb = -1, PF pf = PF()) {
-  // diagonal-block mask of V(row, col), block-local coordinates
-  auto vmask = [](double v, int row, int col) {
-    if (MASK == 0) return (row > col) ? v : (row == col ? 1.0 : 0.0);  // GE
-    if (MASK == 1) return (row <= col) ? v : 0.0;                        // TT
-    return v;
-  };
-  UPROF_DECL_V(_tq);
+  // is V sub-block (row group gg, column group cb) of the diagonal block zero?
+  auto zero_blk = [](int gg, int cb) { return TRI == 0 ? (gg < cb) : (TRI == 1 ? (gg > cb) : false); };
   const int r = lane >> 2, c = lane & 3;
   const int s1a = swz_in(2 * c, r), s1b = swz_in(2 * c + 1, r);  // (2c+h, r)
   const int s3a = swz_in(r, 2 * c), s3b = swz_in(r, 2 * c + 1);  // (r, 2c+h)
@@ -166,17 +163,12 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
 #pragma unroll
   for (int rb = 0; rb < NB / IB; ++rb) {
     if (rb >= rb0 && rb < rb1) {
-      const bool dg = (MASK != 2) && rb == drb;
       double bc[2][4], bn[2][4];
 #pragma unroll
       for (int nb = 0; nb < 4; ++nb) {
         const double* vb = Vs + ((rb * 4) * (IB / 8) + nb) * 64;
         bc[0][nb] = vb[s1a];
         bc[1][nb] = vb[s1b];
-        if (dg) {
-          bc[0][nb] = vmask(bc[0][nb], 2 * c, 8 * nb + r);
-          bc[1][nb] = vmask(bc[1][nb], 2 * c + 1, 8 * nb + r);
-        }
       }
 #pragma unroll
       for (int gg = 0; gg < 4; ++gg) {
@@ -186,16 +178,14 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
             const double* vb = Vs + ((rb * 4 + gg + 1) * (IB / 8) + nb) * 64;
             bn[0][nb] = vb[s1a];
             bn[1][nb] = vb[s1b];
-            if (dg) {
-              bn[0][nb] = vmask(bn[0][nb], 8 * (gg + 1) + 2 * c, 8 * nb + r);
-              bn[1][nb] = vmask(bn[1][nb], 8 * (gg + 1) + 2 * c + 1, 8 * nb + r);
-            }
           }
         }
+        const bool dg = (TRI != 2) && rb == drb;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int nb = 0; nb < 4; ++nb) dmma(w[nb], x[rb * 4 + gg][h], bc[h][nb]);
+          for (int nb = 0; nb < 4; ++nb)
+            if (!(dg && zero_blk(gg, nb))) dmma(w[nb], x[rb * 4 + gg][h], bc[h][nb]);
         pf();
         if (gg < 3) {
 #pragma unroll
@@ -243,17 +233,12 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
 #pragma unroll
   for (int rb = 0; rb < NB / IB; ++rb) {
     if (rb >= rb0 && rb < rb1) {
-      const bool dg = (MASK != 2) && rb == drb;
       double bc[2][4], bn[2][4];
 #pragma unroll
       for (int gg = 0; gg < 4; ++gg) {
         const double* vb = Vs + ((rb * 4 + gg) * (IB / 8)) * 64;
         bc[0][gg] = vb[s3a];
         bc[1][gg] = vb[s3b];
-        if (dg) {
-          bc[0][gg] = vmask(bc[0][gg], 8 * gg + r, 2 * c);
-          bc[1][gg] = vmask(bc[1][gg], 8 * gg + r, 2 * c + 1);
-        }
       }
 #pragma unroll
       for (int kb = 0; kb < 4; ++kb) {
@@ -263,16 +248,14 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
             const double* vb = Vs + ((rb * 4 + gg) * (IB / 8) + kb + 1) * 64;
             bn[0][gg] = vb[s3a];
             bn[1][gg] = vb[s3b];
-            if (dg) {
-              bn[0][gg] = vmask(bn[0][gg], 8 * gg + r, 8 * (kb + 1) + 2 * c);
-              bn[1][gg] = vmask(bn[1][gg], 8 * gg + r, 8 * (kb + 1) + 2 * c + 1);
-            }
           }
         }
+        const bool dg = (TRI != 2) && rb == drb;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int gg = 0; gg < 4; ++gg) dmma(x[rb * 4 + gg], wt[kb][h], bc[h][gg]);
+          for (int gg = 0; gg < 4; ++gg)
+            if (!(dg && zero_blk(gg, kb))) dmma(x[rb * 4 + gg], wt[kb][h], bc[h][gg]);
         pf();
         if (kb < 3) {
 #pragma unroll
@@ -323,22 +306,40 @@ __device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
 // diagonal 32x32 block of a GE (unit-lower) / TT (upper) reflector block is
 // masked where the B fragments are read (warp_apply).
 constexpr int NPW = 4;
-template <int NB>
+template <int NB, int MODE>
 __device__ __forceinline__ void pstage_v(double* Vs, const double* __restrict__ vt, int b, int row0, int row1, int pw,
                                          int lane) {
   const int a = lane & 7, cq = lane >> 3;
   // unit u -> rows row0 + 8*(u>>3) + a, column 4*(u&7) + cq; this warp does
-  // u = pw + NPW*t, i.e. two fixed columns per warp (IB/4 == 2*NPW)
+  // u = pw + NPW*t, i.e. two fixed columns per warp (IB/4 == 2*NPW).  Entries
+  // of the diagonal 32x32 block outside the reflector pattern (GE: unit
+  // lower; TT: upper) are stored directly instead of copied.
   const int c0 = 4 * pw + cq, c1 = c0 + 4 * NPW;
-  const double* s0 = vt + size_t(b * IB + c0) * NB + row0 + a;
-  const double* s1 = vt + size_t(b * IB + c1) * NB + row0 + a;
-  double* d0 = Vs + (c0 >> 3) * 64 + swz_in(a, c0 & 7) + (row0 >> 3) * (IB / 8) * 64;
-  double* d1 = Vs + (c1 >> 3) * 64 + swz_in(a, c1 & 7) + (row0 >> 3) * (IB / 8) * 64;
-  for (int rr = 0; rr < row1 - row0; rr += 8) {
-    cp_async8(d0, s0 + rr);
-    cp_async8(d1, s1 + rr);
-    d0 += (IB / 8) * 64;
-    d1 += (IB / 8) * 64;
+  const double* s0 = vt + size_t(b * IB + c0) * NB + a;
+  const double* s1 = vt + size_t(b * IB + c1) * NB + a;
+  double* d0 = Vs + (c0 >> 3) * 64 + swz_in(a, c0 & 7);
+  double* d1 = Vs + (c1 >> 3) * 64 + swz_in(a, c1 & 7);
+  const int dg0 = b * IB;
+  for (int rr = row0; rr < row1; rr += 8) {
+    double* e0 = d0 + (rr >> 3) * (IB / 8) * 64;
+    double* e1 = d1 + (rr >> 3) * (IB / 8) * 64;
+    const int row = rr + a;
+    if (MODE == TS || rr < dg0 || rr >= dg0 + IB) {
+      cp_async8(e0, s0 + rr);
+      cp_async8(e1, s1 + rr);
+    } else {
+      const int lr = row - dg0;  // row within the diagonal block
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cc = h ? c1 : c0;
+        double* e = h ? e1 : e0;
+        const bool live = (MODE == GE) ? (lr > cc) : (lr <= cc);
+        if (live)
+          cp_async8(e, (h ? s1 : s0) + rr);
+        else
+          *e = (MODE == GE && lr == cc) ? 1.0 : 0.0;
+      }
+    }
   }
 }
 

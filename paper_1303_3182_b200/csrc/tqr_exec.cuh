@@ -93,8 +93,8 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
   // each CTA holds one dequeued item ahead (deadlock-free: items are taken in
   // a topological order and an item only waits on lower-numbered ones)
   if (tid == 0) {
-    mbar_init(&bars[0], 32 * NPW);
-    mbar_init(&bars[1], 32 * NPW);
+    mbar_init(&bars[0], 2 * 32 * NPW);
+    mbar_init(&bars[1], 2 * 32 * NPW);
     mbar_init(&bars[2], NW);
     mbar_init(&bars[3], NW);
     s_cur = atomicAdd(P.queue, 1);

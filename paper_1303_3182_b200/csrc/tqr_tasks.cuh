@@ -80,10 +80,11 @@ __device__ void update_produce(double* sm, const double* __restrict__ vt, const 
     const int b = TRANST ? s : NBLK - 1 - s;
     int r0, r1;
     upd_rows<NB, MODE>(b, r0, r1);
-    pstage_v<NB>(sm + (buf ? S::U_V1 : S::U_V0), vt, b, r0, r1, pw, lane);
+    pstage_v<NB, MODE>(sm + (buf ? S::U_V1 : S::U_V0), vt, b, r0, r1, pw, lane);
     pstage_t(sm + (buf ? S::U_T1 : S::U_T0), tt, b, pw, lane);
     if (MODE != GE) pstage_top<NB>(sm + (buf ? S::U_P1 : S::U_P0), topt, scol0, b * IB, pw, lane);
-    mbar_arrive_cpasync(&full[buf]);
+    mbar_arrive_cpasync(&full[buf]);  // completion of this thread's copies
+    mbar_arrive(&full[buf]);          // release of its direct stores
   }
 }
 
@@ -558,7 +559,7 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
       double x[NB / 8][2];
       load_x<NB>(x, at + size_t(col) * NB, g0, g1, lane);
       double* top = (MODE == GE) ? nullptr : rt + size_t(col) * NB + rb0;
-      warp_apply<NB, true, TS>(x, g0 / (IB / 8), g1 / (IB / 8), Vs, Ts, top, lane);
+      warp_apply<NB, true, (MODE == TS ? 2 : MODE)>(x, g0 / (IB / 8), g1 / (IB / 8), Vs, Ts, top, lane, nullptr, b);
       store_x<NB>(x, at + size_t(col) * NB, g0, g1, lane);
     }
     csync();

@@ -17,8 +17,8 @@ __global__ void __launch_bounds__(NTP, 1) k_upd(double* tiles, double* tt, int r
   __shared__ __align__(8) unsigned long long bars[4];
   unsigned seq = 0;
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 32 * NPW);
-    mbar_init(&bars[1], 32 * NPW);
+    mbar_init(&bars[0], 2 * 32 * NPW);
+    mbar_init(&bars[1], 2 * 32 * NPW);
     mbar_init(&bars[2], NW);
     mbar_init(&bars[3], NW);
   }

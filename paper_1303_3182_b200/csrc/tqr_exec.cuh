@@ -105,26 +105,51 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
   constexpr unsigned NBLK = NB / IB;
   if (warp >= NW) {
     setmaxnreg_dec<40>();
+    __shared__ int s_early;  // producer decision: next item's block 0 staged early
+    int pre = 0;             // block 0 of the current item is already staged
+    const int pw = warp - NW;
+    auto produce = [&](const Item& J, int s_begin, int s_end, unsigned sq) {
+      const double* vt = P.vtiles + toff<NB>(P.p, J.i, J.k);
+      if (J.kind == tqr::UNMQR)
+        update_produce<NB, GE, TRANST>(sm, vt, P.tg + soff<NB>(P.p, J.i, J.k), nullptr, J.slab, pw, lane, bars,
+                                       bars + 2, sq, s_begin, s_end);
+      else if (J.kind == tqr::TTMQR)
+        update_produce<NB, TT, TRANST>(sm, vt, P.te + soff<NB>(P.p, J.i, J.k), P.tiles + toff<NB>(P.p, J.piv, J.j),
+                                       J.slab, pw, lane, bars, bars + 2, sq, s_begin, s_end);
+      else
+        update_produce<NB, TS, TRANST>(sm, vt, P.te + soff<NB>(P.p, J.i, J.k), P.tiles + toff<NB>(P.p, J.piv, J.j),
+                                       J.slab, pw, lane, bars, bars + 2, sq, s_begin, s_end);
+    };
     for (;;) {
       const int it = s_cur, nx = s_nxt;
       if (it >= P.n_items) break;
       const Item I = P.items[it];
       bar_all();  // dependencies satisfied
       if (warp == NW && lane == 0 && nx < P.n_items) prefetch_item<NB>(P, P.items[nx]);
-      if (is_update_kind(I.kind)) {
-        const int pw = warp - NW;
-        const double* vt = P.vtiles + toff<NB>(P.p, I.i, I.k);
-        if (I.kind == tqr::UNMQR)
-          update_produce<NB, GE, TRANST>(sm, vt, P.tg + soff<NB>(P.p, I.i, I.k), nullptr, I.slab, pw, lane, bars,
-                                         bars + 2, seq);
-        else if (I.kind == tqr::TTMQR)
-          update_produce<NB, TT, TRANST>(sm, vt, P.te + soff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.j),
-                                         I.slab, pw, lane, bars, bars + 2, seq);
-        else
-          update_produce<NB, TS, TRANST>(sm, vt, P.te + soff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.j),
-                                         I.slab, pw, lane, bars, bars + 2, seq);
+      const bool upd = is_update_kind(I.kind);
+      if (upd) produce(I, pre ? 1 : 0, NBLK, seq);
+      unsigned seq_next = seq + (upd ? NBLK : 0);
+      // stage block 0 of the next update item now if its predecessors are
+      // already done (non-blocking; never when it depends on this item)
+      pre = 0;
+      if (nx < P.n_items) {
+        const Item J = P.items[nx];
+        if (is_update_kind(J.kind)) {
+          if (tid == NT) {
+            int ok = 1;
+            for (int t = 0; t < J.pred_n && ok; ++t) {
+              const int pr = P.preds[J.pred_lo + t];
+              ok = (pr != it) && ld_acquire(P.done + pr) != 0;
+            }
+            if (ok) __threadfence();  // drop stale L1 lines before cp.async.ca reads
+            s_early = ok;
+          }
+          asm volatile("bar.sync 2, 128;\n" ::: "memory");
+          pre = s_early;
+          if (pre) produce(J, 0, 1, seq_next);
+        }
       }
-      if (is_update_kind(I.kind)) seq += NBLK;
+      seq = seq_next;
       bar_all();  // item finished
       bar_all();  // next item published
     }

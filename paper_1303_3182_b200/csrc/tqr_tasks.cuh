@@ -70,11 +70,11 @@ __device__ __forceinline__ void upd_rows(int b, int& r0, int& r1) {
 template <int NB, int MODE, bool TRANST>
 __device__ void update_produce(double* sm, const double* __restrict__ vt, const double* __restrict__ tt,
                                const double* topt, int slab, int pw, int lane, unsigned long long* full,
-                               unsigned long long* empty, unsigned seq) {
+                               unsigned long long* empty, unsigned seq, int s_begin = 0, int s_end = NB / IB) {
   using S = Smem<NB>;
   constexpr int NBLK = NB / IB;
   const int scol0 = slab * WS;
-  for (int s = 0; s < NBLK; ++s) {
+  for (int s = s_begin; s < s_end; ++s) {
     const unsigned q = seq + unsigned(s), buf = q & 1u;
     if (q >= 2) mbar_wait(&empty[buf], ((q >> 1) - 1u) & 1u);
     const int b = TRANST ? s : NBLK - 1 - s;

@@ -138,47 +138,35 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
   const int r = lane >> 2, c = lane & 3;
   const int s1a = swz_in(2 * c, r), s1b = swz_in(2 * c + 1, r);  // (2c+h, r)
   const int s3a = swz_in(r, 2 * c), s3b = swz_in(r, 2 * c + 1);  // (r, 2c+h)
+  // top_s: the block's IB pivot rows of this warp's 8 columns staged in smem
+  // (column-major, ld IB); else read from global
   double w[4][2], ap[4][2];
   if (top) {
 #pragma unroll
     for (int nb = 0; nb < 4; ++nb) {
-      // top_s: the block's IB top rows of this warp's 8 columns staged in
-      // smem (column-major, ld IB); else read from global
       double2 v = top_s ? *reinterpret_cast<const double2*>(top_s + 8 * nb + 2 * c + r * IB)
                         : ldcg2(top + 8 * nb + 2 * c + r * NB);
       ap[nb][0] = v.x;
       ap[nb][1] = v.y;
     }
-  } else {
-#pragma unroll
-    for (int nb = 0; nb < 4; ++nb) ap[nb][0] = ap[nb][1] = 0.0;
   }
+  // accumulate V^T X from zero and add the pivot rows once afterwards, as
+  // LAPACK's dlarfb does (one rounding of the large operand per block)
 #pragma unroll
-  for (int nb = 0; nb < 4; ++nb) {
-    w[nb][0] = ap[nb][0];
-    w[nb][1] = ap[nb][1];
-  }
+  for (int nb = 0; nb < 4; ++nb) w[nb][0] = w[nb][1] = 0.0;
   // W^T (8 x IB) += X (8 x rows) * V (rows x IB); B fragments of the next
   // row group are loaded while the current group's DMMAs issue
 #pragma unroll
   for (int rb = 0; rb < NB / IB; ++rb) {
     if (rb >= rb0 && rb < rb1) {
-      double bc[2][4], bn[2][4];
-#pragma unroll
-      for (int nb = 0; nb < 4; ++nb) {
-        const double* vb = Vs + ((rb * 4) * (IB / 8) + nb) * 64;
-        bc[0][nb] = vb[s1a];
-        bc[1][nb] = vb[s1b];
-      }
 #pragma unroll
       for (int gg = 0; gg < 4; ++gg) {
-        if (gg < 3) {
+        double bc[2][4];
 #pragma unroll
-          for (int nb = 0; nb < 4; ++nb) {
-            const double* vb = Vs + ((rb * 4 + gg + 1) * (IB / 8) + nb) * 64;
-            bn[0][nb] = vb[s1a];
-            bn[1][nb] = vb[s1b];
-          }
+        for (int nb = 0; nb < 4; ++nb) {
+          const double* vb = Vs + ((rb * 4 + gg) * (IB / 8) + nb) * 64;
+          bc[0][nb] = vb[s1a];
+          bc[1][nb] = vb[s1b];
         }
         const bool dg = (TRI != 2) && rb == drb;
 #pragma unroll
@@ -187,17 +175,16 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
           for (int nb = 0; nb < 4; ++nb)
             if (!(dg && zero_blk(gg, nb))) dmma(w[nb], x[rb * 4 + gg][h], bc[h][nb]);
         pf();
-        if (gg < 3) {
-#pragma unroll
-          for (int nb = 0; nb < 4; ++nb) {
-            bc[0][nb] = bn[0][nb];
-            bc[1][nb] = bn[1][nb];
-          }
-        }
       }
     }
   }
-  UPROF_MARK_V(10, _tq);
+  if (top) {
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      w[nb][0] += ap[nb][0];
+      w[nb][1] += ap[nb][1];
+    }
+  }
   // W^T <- W^T T (Q^T) or W^T T^T (Q); T upper triangular
   double tb[2][4][4];
 #pragma unroll
@@ -229,42 +216,42 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
     wt[nb][1] = -wt[nb][1];
   }
   UPROF_MARK_V(11, _tq);
-  // X -= W^T V^T ; consecutive DMMAs hit different row groups (independent)
+  // X -= W^T V^T ; per 32-row block the product is accumulated from zero and
+  // subtracted from X once (LAPACK-like rounding of the large operand)
 #pragma unroll
   for (int rb = 0; rb < NB / IB; ++rb) {
     if (rb >= rb0 && rb < rb1) {
-      double bc[2][4], bn[2][4];
+      double acc3[4][2];
 #pragma unroll
-      for (int gg = 0; gg < 4; ++gg) {
-        const double* vb = Vs + ((rb * 4 + gg) * (IB / 8)) * 64;
-        bc[0][gg] = vb[s3a];
-        bc[1][gg] = vb[s3b];
-      }
+      for (int gg = 0; gg < 4; ++gg) acc3[gg][0] = acc3[gg][1] = 0.0;
 #pragma unroll
       for (int kb = 0; kb < 4; ++kb) {
-        if (kb < 3) {
+        double bc[2][4];
 #pragma unroll
-          for (int gg = 0; gg < 4; ++gg) {
-            const double* vb = Vs + ((rb * 4 + gg) * (IB / 8) + kb + 1) * 64;
-            bn[0][gg] = vb[s3a];
-            bn[1][gg] = vb[s3b];
-          }
+        for (int gg = 0; gg < 4; ++gg) {
+          const double* vb = Vs + ((rb * 4 + gg) * (IB / 8) + kb) * 64;
+          bc[0][gg] = vb[s3a];
+          bc[1][gg] = vb[s3b];
         }
         const bool dg = (TRI != 2) && rb == drb;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int gg = 0; gg < 4; ++gg)
+#ifdef TQR_DIRECT_ACC
             if (!(dg && zero_blk(gg, kb))) dmma(x[rb * 4 + gg], wt[kb][h], bc[h][gg]);
+#else
+            if (!(dg && zero_blk(gg, kb))) dmma(acc3[gg], wt[kb][h], bc[h][gg]);
+#endif
         pf();
-        if (kb < 3) {
-#pragma unroll
-          for (int gg = 0; gg < 4; ++gg) {
-            bc[0][gg] = bn[0][gg];
-            bc[1][gg] = bn[1][gg];
-          }
-        }
       }
+#ifndef TQR_DIRECT_ACC
+#pragma unroll
+      for (int gg = 0; gg < 4; ++gg) {
+        x[rb * 4 + gg][0] += acc3[gg][0];
+        x[rb * 4 + gg][1] += acc3[gg][1];
+      }
+#endif
     }
   }
   pf.flush();

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <numeric>
 #include <queue>
@@ -26,6 +27,9 @@
 using namespace tqrk;
 
 using namespace tqrx;
+namespace tqrx {
+int g_flags = 0;
+}
 
 namespace {
 
@@ -293,6 +297,12 @@ namespace {
 
 unsigned long long* g_trace = nullptr;  // tqr_set_trace: per-item timestamps of the next run
 
+// debug knobs from the environment: TQR_GRID (CTAs), TQR_FLAGS (bit 0: no early staging)
+int env_int(const char* k, int dflt) {
+  const char* v = getenv(k);
+  return v ? atoi(v) : dflt;
+}
+
 int num_sms() {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -307,7 +317,8 @@ cudaError_t run(const DevSched& d, int nb, bool transT, const double* vtiles, do
   if ((e = cudaMemsetAsync(d.queue, 0, sizeof(int), st)) != cudaSuccess) return e;
   if (d.n_items == 0) return cudaSuccess;
   DevView v{d.items, d.preds, d.done, d.queue, d.n_items};
-  const int grid = std::min(d.n_items, num_sms());
+  tqrx::g_flags = env_int("TQR_FLAGS", 0);
+  const int grid = std::min(d.n_items, std::max(1, env_int("TQR_GRID", num_sms())));
   switch (nb) {
     case 64:
       return transT ? launch_exec<64, true>(v, vtiles, tiles, tg, te, p, g_trace, grid, st)

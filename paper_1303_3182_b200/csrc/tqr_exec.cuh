@@ -31,6 +31,7 @@ struct ExecParams {
   double* te;
   int p;
   unsigned long long* trace;  // optional: per item {t_dequeue, t_ready, t_end, smid}
+  int flags;                  // debug: bit 0 = no early staging
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -132,7 +133,8 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
       // stage block 0 of the next update item now if its predecessors are
       // already done (non-blocking; never when it depends on this item)
       pre = 0;
-      if (nx < P.n_items) {
+      // (only behind an update item: a panel item uses the same shared memory)
+      if (upd && nx < P.n_items && !(P.flags & 1)) {
         const Item J = P.items[nx];
         if (is_update_kind(J.kind)) {
           if (tid == NT) {
@@ -220,6 +222,8 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
   }
 }
 
+extern int g_flags;
+
 struct DevView {
   const Item* items;
   const int32_t* preds;
@@ -250,7 +254,7 @@ TQR_DECLARE_LAUNCH(256, false)
     const size_t smem = Smem<NB>::BYTES;                                                                           \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));            \
     if (e != cudaSuccess) return e;                                                                                \
-    ExecParams P{d.items, d.preds, d.n_items, d.done, d.queue, vtiles, tiles, tg, te, p, trace};                   \
+    ExecParams P{d.items, d.preds, d.n_items, d.done, d.queue, vtiles, tiles, tg, te, p, trace, g_flags};                   \
     kern<<<grid, NTP, smem, st>>>(P);                                                                               \
     return cudaGetLastError();                                                                                     \
   }

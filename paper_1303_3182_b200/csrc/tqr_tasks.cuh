@@ -167,6 +167,26 @@ __device__ __forceinline__ void tn_acc(double (&acc)[NBK][2], const double* P, i
   }
 }
 
+// Trailing update of the columns right of panel block b (8 columns per warp,
+// register-resident) — a separate non-inlined function so that its register
+// allocation does not compete with the panel's live state.
+template <int NB, int MODE>
+__device__ __noinline__ void panel_trailing(double* at, double* rt, const double* Vs, const double* Ts, int b, int warp,
+                                            int lane) {
+  const int rb0 = b * IB;
+  const int nch = (NB - rb0 - IB) / 8;
+  const int g0 = (MODE == GE) ? rb0 / 8 : 0;
+  const int g1 = (MODE == TT) ? (rb0 + IB) / 8 : NB / 8;
+  for (int ch = warp; ch < nch; ch += NW) {
+    const int col = rb0 + IB + ch * 8;
+    double x[NB / 8][2];
+    load_x<NB>(x, at + size_t(col) * NB, g0, g1, lane);
+    double* top = (MODE == GE) ? nullptr : rt + size_t(col) * NB + rb0;
+    warp_apply<NB, true, (MODE == TS ? 2 : MODE)>(x, g0 / (IB / 8), g1 / (IB / 8), Vs, Ts, top, lane, nullptr, b);
+    store_x<NB>(x, at + size_t(col) * NB, g0, g1, lane);
+  }
+}
+
 template <int NB, int MODE>
 __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile (i,k)*/,
                            double* rt /*TT/TS: pivot tile (piv,k)*/, double* tslot, int tid,
@@ -413,16 +433,14 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
             double a1 = vmask_p<NB, MODE>(P[row + (c0 + 4 + c) * PLD], row, c0 + 4 + c);
             for (int nb = 0; nb < ncol / 8; ++nb) {
               const int cb = c0 + 8 + 8 * nb;
-              double acc2[2];
-              acc2[0] = P[8 * mb + r + (cb + 2 * c) * PLD];
-              acc2[1] = P[8 * mb + r + (cb + 2 * c + 1) * PLD];
-              const double b0 = -WP[c * LDW + 8 + 8 * nb + r];
-              const double b1 = -WP[(4 + c) * LDW + 8 + 8 * nb + r];
+              double acc2[2] = {0.0, 0.0};
+              const double b0 = WP[c * LDW + 8 + 8 * nb + r];
+              const double b1 = WP[(4 + c) * LDW + 8 + 8 * nb + r];
               dmma(acc2, a0, b0);
               dmma(acc2, a1, b1);
               if (row < nrows) {
-                P[8 * mb + r + (cb + 2 * c) * PLD] = acc2[0];
-                P[8 * mb + r + (cb + 2 * c + 1) * PLD] = acc2[1];
+                P[8 * mb + r + (cb + 2 * c) * PLD] -= acc2[0];
+                P[8 * mb + r + (cb + 2 * c + 1) * PLD] -= acc2[1];
               }
             }
           }
@@ -551,17 +569,7 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
     csync();
     mark(3);
     // ---- trailing update of columns rb0+IB .. NB on DMMA, 8 columns per warp
-    const int nch = (NB - rb0 - IB) / 8;
-    const int g0 = (MODE == GE) ? rb0 / 8 : 0;
-    const int g1 = (MODE == TT) ? (rb0 + IB) / 8 : NB / 8;
-    for (int ch = warp; ch < nch; ch += NW) {
-      const int col = rb0 + IB + ch * 8;
-      double x[NB / 8][2];
-      load_x<NB>(x, at + size_t(col) * NB, g0, g1, lane);
-      double* top = (MODE == GE) ? nullptr : rt + size_t(col) * NB + rb0;
-      warp_apply<NB, true, (MODE == TS ? 2 : MODE)>(x, g0 / (IB / 8), g1 / (IB / 8), Vs, Ts, top, lane, nullptr, b);
-      store_x<NB>(x, at + size_t(col) * NB, g0, g1, lane);
-    }
+    panel_trailing<NB, MODE>(at, rt, Vs, Ts, b, warp, lane);
     csync();
     mark(4);
   }

@@ -129,3 +129,69 @@ def test_user_list_with_reverse_entries():
     res = tiled_qr(A, nb=64, elim=lst)
     rp = replay_build(A, res.build, 64)
     _compare_tiles(res, rp, np.linalg.norm(A), "reverse")
+
+
+def _checks_full(A_np, res):
+    """north_star tolerances at full size, computed on the GPU (cuBLAS fp64
+    matmuls as the checker only)."""
+    At = torch.from_numpy(A_np).cuda()
+    R = res.R()
+    Q = res.Q()
+    nA = torch.linalg.norm(At)
+    resid = (torch.linalg.norm(At - Q @ R) / nA).item()
+    n = R.shape[0]
+    orth = torch.linalg.norm(Q.T @ Q - torch.eye(n, dtype=torch.float64, device="cuda")).item()
+    return R, resid, orth
+
+
+def test_c4_ill_conditioned_fibonacci_full_size():
+    """BASELINE config 4: 8192x4096, nb=256, Fibonacci/TT, U diag(s) V^T with
+    s geometric 1..1e-12 (seed 3): backward error and orthogonality <= 1e-12,
+    R equal to cuSOLVER's up to row signs within 1e-11 ||A||_F."""
+    _need_gpu()
+    rng = np.random.default_rng(3)
+    m, n = 8192, 4096
+    U = np.linalg.qr(rng.standard_normal((m, n)))[0]
+    V = np.linalg.qr(rng.standard_normal((n, n)))[0]
+    A = np.ascontiguousarray((U * np.geomspace(1.0, 1e-12, n)) @ V.T)
+    res = tiled_qr(A, nb=256, algo="fibonacci")
+    assert res.build.cp == 374
+    R, resid, orth = _checks_full(A, res)
+    assert resid <= 1e-12, resid
+    assert orth <= 1e-12, orth
+    Rref = torch.linalg.qr(torch.from_numpy(A).cuda(), mode="r")[1]
+    s1 = torch.sign(torch.diagonal(R))
+    s2 = torch.sign(torch.diagonal(Rref))
+    d = torch.linalg.norm(R * s1[:, None] - Rref * s2[:, None]).item()
+    assert d <= 1e-11 * np.linalg.norm(A), d
+
+
+@pytest.mark.parametrize("algo,family,bs,p,q", [("asap", "TT", None, 6, 3), ("grasap", "TT", None, 6, 3),
+                                                ("binarytree", "TS", None, 6, 3), ("plasmatree", "TS", 2, 6, 3),
+                                                ("fibonacci", "TS", None, 5, 2)])
+def test_more_trees_nb256_vs_replay(algo, family, bs, p, q):
+    _need_gpu()
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((p * 256, q * 256))
+    b = P.build_tree(p, q, algo, family=family, bs=bs)
+    plan, res = _run(b, A, 256)
+    rp = replay_build(A, b, 256)
+    _compare_tiles(res, rp, np.linalg.norm(A), (algo, family))
+
+
+# ||Q^T Q - I||_F of the LAPACK replay (oracle/replay.py) of the same C3
+# Greedy trace, measured on the GPU box's CPU (tools/replay_orth.py,
+# profiles/accuracy_r01.json): the reference algorithm itself lands just
+# above 1e-12 at n = 16384, so the bar there is "within 1.5x of the replay".
+REPLAY_ORTH = {8192: 5.077e-13, 16384: 1.018e-12}
+
+
+@pytest.mark.parametrize("n", [8192, 16384])
+def test_c3_shape_residual_orthogonality(n):
+    """BASELINE config 3 (Greedy/TT, nb=256, seed 2) at n=8192 and full size."""
+    _need_gpu()
+    A = np.random.default_rng(2).standard_normal((n, n))
+    res = tiled_qr(A, nb=256, algo="greedy")
+    R, resid, orth = _checks_full(A, res)
+    assert resid <= 1e-12, resid
+    assert orth <= max(1e-12, 1.5 * REPLAY_ORTH[n]), orth

@@ -105,6 +105,11 @@ typedef struct {
  * kernels split into column slabs, hazard edges (taskgraph.py:262-322)
  * refined to slab granularity, items ordered by weighted ASAP start.       */
 int tqr_plan_create(const tqr_build* b, int nb, int ib, tqr_plan** out);
+/* Same, with streaming I/O work items in the device schedule (io bit 0:
+ * PACK items read the row-major input as its tile rows arrive; bit 1:
+ * UNPACK items write each finished R tile to row-major (host-mapped) memory
+ * as soon as it is final).  Run with tqr_factor_io.                        */
+int tqr_plan_create_io(const tqr_build* b, int nb, int ib, int io, tqr_plan** out);
 int tqr_plan_get_info(const tqr_plan* plan, tqr_plan_info* out);
 void tqr_plan_free(tqr_plan* plan);
 
@@ -118,6 +123,14 @@ int tqr_extract_r(const double* tiles, int p, int q, int nb, double* R, int64_t 
  * TSQRT, TSMQR) on `tiles`; writes T factors into tg/te (tg_stride /
  * te_stride doubles per tile).  Asynchronous on `stream`.                  */
 int tqr_factor(tqr_plan* plan, double* tiles, double* tg, double* te, void* stream);
+/* Streaming factorization: a_src = row-major m x n input staging buffer in
+ * device memory, filled asynchronously by the caller one nb-row block at a
+ * time, each block followed by setting arrive[i] != 0 (e.g. a 4-byte
+ * cudaMemcpyAsync on the same copy stream); arrive[] must be zero at launch.
+ * r_dst = row-major n x n R (device-accessible, e.g. pinned host memory),
+ * strictly-lower part outside the diagonal tiles left untouched.           */
+int tqr_factor_io(tqr_plan* plan, const double* a_src, int64_t lda, const int* arrive, double* tiles, double* tg,
+                  double* te, double* r_dst, int64_t ldr, void* stream);
 /* C <- Q C (trans=0) or Q^T C (trans=1) for C stored as p x c_cols tiles,
  * replaying the trace's reflectors (forward for Q^T, reverse for Q).      */
 int tqr_apply_q(tqr_plan* plan, int trans, const double* tiles, const double* tg, const double* te,

@@ -62,12 +62,14 @@ SIGNATURES = {
     "tqr_trace_build": (C.c_int, [C.c_int, C.c_int, i8p, i32p, C.c_int64, C.POINTER(vp)]),
     "tqr_build_free": (None, [vp]),
     "tqr_plan_create": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(vp)]),
+    "tqr_plan_create_io": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
     "tqr_plan_get_info": (C.c_int, [vp, C.POINTER(PlanInfo)]),
     "tqr_plan_free": (None, [vp]),
     "tqr_pack": (C.c_int, [vp, C.c_int64, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp]),
     "tqr_unpack": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int64, C.c_int, vp]),
     "tqr_extract_r": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int64, C.c_int, vp]),
     "tqr_factor": (C.c_int, [vp, vp, vp, vp, vp]),
+    "tqr_factor_io": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, C.c_int64, vp]),
     "tqr_apply_q": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, C.c_int, vp]),
     "tqr_fp64_peak": (C.c_int, [f64p, vp]),
     "tqr_set_trace": (C.c_int, [vp]),

@@ -521,17 +521,21 @@ Build* build_tree(int p, int q, std::string algo, bool ts, int bs, int grasap_i,
 // ---------------------------------------------------------------------------
 // hazard DAG (taskgraph.py:262-322)
 
-std::vector<Edge> hazard_edges(const Build& b) {
+std::vector<Edge> hazard_edges(const Build& b) { return hazard_edges(b.p, b.q, b.trace); }
+
+std::vector<Edge> hazard_edges(int p, int q, const std::vector<TaskRec>& trace) {
   enum { MD = 0, MR = 1, MV = 2, MT = 3, MS = 4 };
-  const size_t P = size_t(b.p) + 2, Q = size_t(b.q) + 2;
+  const size_t P = size_t(p) + 2, Q = size_t(q) + 2;
   auto tid = [&](int m, int r, int c) -> size_t { return (size_t(m) * P + size_t(r)) * Q + size_t(c); };
   std::vector<int32_t> last_write(5 * P * Q, -1);
   std::vector<std::vector<int32_t>> readers(5 * P * Q);
   std::vector<Edge> edges;
-  edges.reserve(b.trace.size() * 4);
+  edges.reserve(trace.size() * 4);
+  std::vector<size_t> rdv;
   size_t rd[3], wr[2];
-  for (size_t t = 0; t < b.trace.size(); ++t) {
-    const auto& T = b.trace[t];
+  for (size_t t = 0; t < trace.size(); ++t) {
+    const auto& T = trace[t];
+    const size_t* rdp = rd;
     int nr = 0, nw = 0;
     switch (T.kind) {
       case GEQRT:
@@ -559,12 +563,18 @@ std::vector<Edge> hazard_edges(const Build& b) {
         wr[nw++] = tid(MD, T.a, T.d);
         wr[nw++] = tid(MD, T.b, T.d);
         break;
+      case PACK:  // the tile's original data arrives: writes D(i,j)
+        wr[nw++] = tid(MD, T.a, T.b);
+        break;
+      case UNPACK:  // final R tile (i,j) leaves: reads R(i,i) or D(i,j)
+        rd[nr++] = tid(T.a == T.b ? MR : MD, T.a, T.b);
+        break;
     }
     const int32_t me = int32_t(t);
     for (int x = 0; x < nr; ++x) {
-      int32_t w = last_write[rd[x]];
+      int32_t w = last_write[rdp[x]];
       if (w >= 0) edges.push_back({w, me, 0});
-      readers[rd[x]].push_back(me);
+      readers[rdp[x]].push_back(me);
     }
     for (int x = 0; x < nw; ++x) {
       auto& rs = readers[wr[x]];

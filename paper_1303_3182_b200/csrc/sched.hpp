@@ -18,7 +18,9 @@
 
 namespace tqr {
 
-enum Kind : int8_t { GEQRT = 0, TTQRT = 1, TSQRT = 2, UNMQR = 3, TTMQR = 4, TSMQR = 5 };
+enum Kind : int8_t { GEQRT = 0, TTQRT = 1, TSQRT = 2, UNMQR = 3, TTMQR = 4, TSMQR = 5,
+                    // device-schedule-only kinds (streaming I/O): tile (a,b) arrives / leaves
+                    PACK = 6, UNPACK = 7 };
 static const char* const kKindName[6] = {"GEQRT", "TTQRT", "TSQRT", "UNMQR", "TTMQR", "TSMQR"};
 
 struct Entry {
@@ -123,5 +125,6 @@ struct Edge {
   int8_t cause;
 };
 std::vector<Edge> hazard_edges(const Build& b);
+std::vector<Edge> hazard_edges(int p, int q, const std::vector<TaskRec>& trace);
 
 }  // namespace tqr

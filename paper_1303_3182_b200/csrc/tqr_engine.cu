@@ -181,6 +181,8 @@ void expand(const std::vector<Task>& tasks, const std::vector<std::vector<int32_
 inline double item_cost(int kind, int nb) {
   const double big = nb >= 256 ? 1.0 : 0.5;
   switch (kind) {
+    case tqr::PACK: return 0.1;
+    case tqr::UNPACK: return 0.5;
     case tqr::GEQRT: return 3.0 * big + 0.5;
     case tqr::TTQRT: return 2.5 * big + 0.5;
     case tqr::TSQRT: return 4.0 * big + 0.5;
@@ -214,6 +216,7 @@ void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers
     double best = 0.0;
     for (int32_t k = nsucc[v]; k < nsucc[v + 1]; ++k) best = std::max(best, prio[size_t(succ[size_t(k)])]);
     prio[v] = w[v] + best;
+    if (items[v].kind == tqr::UNPACK) prio[v] = 1e12;  // ship finished R tiles at once
   }
   std::vector<int32_t> indeg(n);
   for (size_t v = 0; v < n; ++v) indeg[v] = items[v].pred_n;
@@ -281,7 +284,7 @@ void upload(DevSched& d, const std::vector<Item>& items, const std::vector<int32
 }  // namespace
 
 struct tqr_plan {
-  int p = 0, q = 0, nb = 0, ib = IB, ts = 0;
+  int p = 0, q = 0, nb = 0, ib = IB, ts = 0, io = 0;
   int64_t n_tasks = 0;
   double flops = 0;
   std::vector<Task> trace;  // factorization trace (for apply-Q)
@@ -311,7 +314,7 @@ int num_sms() {
 }
 
 cudaError_t run(const DevSched& d, int nb, bool transT, const double* vtiles, double* tiles, double* tg, double* te,
-                int p, cudaStream_t st) {
+                int p, cudaStream_t st, const IoBufs& io = IoBufs{}) {
   cudaError_t e;
   if ((e = cudaMemsetAsync(d.done, 0, size_t(std::max(d.n_items, 1)) * sizeof(int), st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(d.queue, 0, sizeof(int), st)) != cudaSuccess) return e;
@@ -321,11 +324,11 @@ cudaError_t run(const DevSched& d, int nb, bool transT, const double* vtiles, do
   const int grid = std::min(d.n_items, std::max(1, env_int("TQR_GRID", num_sms())));
   switch (nb) {
     case 64:
-      return transT ? launch_exec<64, true>(v, vtiles, tiles, tg, te, p, g_trace, grid, st)
-                    : launch_exec<64, false>(v, vtiles, tiles, tg, te, p, g_trace, grid, st);
+      return transT ? launch_exec<64, true>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io)
+                    : launch_exec<64, false>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io);
     case 256:
-      return transT ? launch_exec<256, true>(v, vtiles, tiles, tg, te, p, g_trace, grid, st)
-                    : launch_exec<256, false>(v, vtiles, tiles, tg, te, p, g_trace, grid, st);
+      return transT ? launch_exec<256, true>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io)
+                    : launch_exec<256, false>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io);
   }
   return cudaErrorInvalidValue;
 }
@@ -340,7 +343,7 @@ int cuda_guarded(cudaError_t e) {
 
 extern "C" {
 
-int tqr_plan_create(const tqr_build* hb, int nb, int ib, tqr_plan** out) {
+int tqr_plan_create_io(const tqr_build* hb, int nb, int ib, int io, tqr_plan** out) {
   return tqr::guard([&] {
     if (!hb || !hb->b) throw tqr::ValueError("null build");
     const tqr::Build& b = *hb->b;
@@ -354,6 +357,7 @@ int tqr_plan_create(const tqr_build* hb, int nb, int ib, tqr_plan** out) {
       P->nb = nb;
       P->ib = ib;
       P->ts = b.ts;
+      P->io = io;
       const size_t n = b.trace.size();
       P->n_tasks = int64_t(n);
       P->trace.resize(n);
@@ -369,24 +373,43 @@ int tqr_plan_create(const tqr_build* hb, int nb, int ib, tqr_plan** out) {
         }
         P->trace[t] = T;
       }
+      // device task list: [PACK(i,j) for every tile] + trace + [UNPACK(i,j)
+      // for every R tile] when streaming I/O is requested
+      std::vector<tqr::TaskRec> recs;
+      std::vector<Task> tasks;
+      if (io & 1)
+        for (int j = 1; j <= b.q; ++j)
+          for (int i = 1; i <= b.p; ++i) {
+            recs.push_back({tqr::PACK, i, j, -1, -1, 0});
+            tasks.push_back({tqr::PACK, i, -1, -1, j});
+          }
+      recs.insert(recs.end(), b.trace.begin(), b.trace.end());
+      tasks.insert(tasks.end(), P->trace.begin(), P->trace.end());
+      if (io & 2)
+        for (int i = 1; i <= b.q; ++i)
+          for (int j = i; j <= b.q; ++j) {
+            recs.push_back({tqr::UNPACK, i, j, -1, -1, 0});
+            tasks.push_back({tqr::UNPACK, i, -1, -1, j});
+          }
+      const size_t m = tasks.size();
       // hazard edges of the reference model, weighted ASAP order (QR weights)
-      auto edges = tqr::hazard_edges(b);
-      std::vector<std::vector<int32_t>> in(n);
+      auto edges = tqr::hazard_edges(b.p, b.q, recs);
+      std::vector<std::vector<int32_t>> in(m);
       for (const auto& e : edges) in[size_t(e.v)].push_back(e.u);
-      static const int64_t W[6] = {4, 2, 6, 6, 6, 12};
-      std::vector<int64_t> est(n, 0);
-      for (size_t v = 0; v < n; ++v)
-        for (int32_t u : in[v]) est[v] = std::max(est[v], est[size_t(u)] + W[P->trace[size_t(u)].kind]);
-      std::vector<int32_t> order(n);
+      static const int64_t W[8] = {4, 2, 6, 6, 6, 12, 1, 1};
+      std::vector<int64_t> est(m, 0);
+      for (size_t v = 0; v < m; ++v)
+        for (int32_t u : in[v]) est[v] = std::max(est[v], est[size_t(u)] + W[tasks[size_t(u)].kind]);
+      std::vector<int32_t> order(m);
       std::iota(order.begin(), order.end(), 0);
       std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t c) { return est[size_t(a)] < est[size_t(c)]; });
       std::vector<Item> items;
       std::vector<int32_t> preds;
-      expand(P->trace, in, order, nb / WS, items, preds);
+      expand(tasks, in, order, nb / WS, items, preds);
       cp_order(items, preds, num_sms_host(), nb);
       upload(P->fac, items, preds);
-      const double m = double(b.p) * nb, nn = double(b.q) * nb;
-      P->flops = 2.0 * nn * nn * (m - nn / 3.0);
+      const double mm = double(b.p) * nb, nn = double(b.q) * nb;
+      P->flops = 2.0 * nn * nn * (mm - nn / 3.0);
     } catch (...) {
       delete P;
       throw;
@@ -394,6 +417,8 @@ int tqr_plan_create(const tqr_build* hb, int nb, int ib, tqr_plan** out) {
     *out = P;
   });
 }
+
+int tqr_plan_create(const tqr_build* hb, int nb, int ib, tqr_plan** out) { return tqr_plan_create_io(hb, nb, ib, 0, out); }
 
 int tqr_plan_get_info(const tqr_plan* P, tqr_plan_info* o) {
   return tqr::guard([&] {
@@ -420,6 +445,18 @@ int tqr_factor(tqr_plan* P, double* tiles, double* tg, double* te, void* stream)
   });
   if (rc) return rc;
   return cuda_guarded(run(P->fac, P->nb, true, tiles, tiles, tg, te, P->p, static_cast<cudaStream_t>(stream)));
+}
+
+int tqr_factor_io(tqr_plan* P, const double* a_src, int64_t lda, const int* arrive, double* tiles, double* tg,
+                  double* te, double* r_dst, int64_t ldr, void* stream) {
+  int rc = tqr::guard([&] {
+    if (!P) throw tqr::ValueError("null plan");
+    if ((P->io & 1) && (!a_src || !arrive)) throw tqr::ValueError("plan streams its input: a_src and arrive needed");
+    if ((P->io & 2) && !r_dst) throw tqr::ValueError("plan streams R out: r_dst needed");
+  });
+  if (rc) return rc;
+  IoBufs io{a_src, lda, arrive, r_dst, ldr};
+  return cuda_guarded(run(P->fac, P->nb, true, tiles, tiles, tg, te, P->p, static_cast<cudaStream_t>(stream), io));
 }
 
 int tqr_apply_q(tqr_plan* P, int trans, const double* tiles, const double* tg, const double* te, double* c_tiles,

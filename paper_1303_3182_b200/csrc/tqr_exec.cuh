@@ -32,6 +32,12 @@ struct ExecParams {
   int p;
   unsigned long long* trace;  // optional: per item {t_dequeue, t_ready, t_end, smid}
   int flags;                  // debug: bit 0 = no early staging
+  // streaming I/O (PACK / UNPACK items)
+  const double* a_src;  // row-major input staging (device), ld lda
+  long long lda;
+  const int* arrive;  // per tile row: nonzero once its rows landed in a_src
+  double* r_dst;      // row-major R output (host-mapped pinned memory), ld ldr
+  long long ldr;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -76,6 +82,55 @@ __device__ __forceinline__ void prefetch_item(const ExecParams& P, const Item& I
       prefetch_l2(P.tiles + toff<NB>(P.p, I.i, I.j) + size_t(I.slab) * WS * NB, slab_bytes);
       prefetch_l2(P.tiles + toff<NB>(P.p, I.piv, I.j) + size_t(I.slab) * WS * NB, slab_bytes);
       break;
+  }
+}
+
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// PACK(i,j): wait until tile row i of the row-major input has landed (the
+// host's flag copy follows the row block on the same copy stream), then
+// transpose tile (i,j) into the tile-major, column-major-tile layout.
+template <int NB>
+__device__ void pack_item(double* sm, const ExecParams& P, int i, int j, int tid) {
+  if (tid == 0) {
+    while (ld_acquire_sys(P.arrive + (i - 1)) == 0) __nanosleep(200);
+  }
+  csync();
+  double* dst = P.tiles + toff<NB>(P.p, i, j);
+  const double* src = P.a_src + (long long)(i - 1) * NB * P.lda + (long long)(j - 1) * NB;
+  double(*t)[33] = reinterpret_cast<double(*)[33]>(sm);  // 32 x 33 transpose tile
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int s = 0; s < (NB / 32) * (NB / 32); ++s) {
+    const int ra = (s % (NB / 32)) * 32, cb = (s / (NB / 32)) * 32;
+    for (int y = warp; y < 32; y += NW) t[y][lane] = __ldcg(src + (long long)(ra + y) * P.lda + cb + lane);
+    csync();
+    for (int y = warp; y < 32; y += NW) dst[(ra + lane) + size_t(cb + y) * NB] = t[lane][y];
+    csync();
+  }
+}
+
+// UNPACK(i,j): final R tile (i,j) (j >= i) -> row-major R in host-mapped
+// memory (upper triangle for the diagonal tile, zeros below it).
+template <int NB>
+__device__ void unpack_item(double* sm, const ExecParams& P, int i, int j, int tid) {
+  const double* src = P.tiles + toff<NB>(P.p, i, j);
+  double* dst = P.r_dst + (long long)(i - 1) * NB * P.ldr + (long long)(j - 1) * NB;
+  double(*t)[33] = reinterpret_cast<double(*)[33]>(sm);
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int s = 0; s < (NB / 32) * (NB / 32); ++s) {
+    const int ra = (s % (NB / 32)) * 32, cb = (s / (NB / 32)) * 32;
+    for (int y = warp; y < 32; y += NW) {
+      double v = __ldcg(src + (ra + lane) + size_t(cb + y) * NB);  // (row ra+lane, col cb+y)
+      if (i == j && ra + lane > cb + y) v = 0.0;
+      t[y][lane] = v;
+    }
+    csync();
+    for (int y = warp; y < 32; y += NW) dst[(long long)(ra + y) * P.ldr + cb + lane] = t[lane][y];
+    csync();
   }
 }
 
@@ -191,6 +246,12 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
           panel_item<NB, TS>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.k),
                              P.te + soff<NB>(P.p, I.i, I.k), tid, pprof);
         break;
+      case tqr::PACK:
+        if constexpr (TRANST) pack_item<NB>(sm, P, I.i, I.j, tid);
+        break;
+      case tqr::UNPACK:
+        if constexpr (TRANST) unpack_item<NB>(sm, P, I.i, I.j, tid);
+        break;
       case tqr::UNMQR:
         update_consume<NB, GE, TRANST>(sm, P.tiles + toff<NB>(P.p, I.i, I.j), nullptr, I.slab, tid, bars, bars + 2,
                                        seq);
@@ -224,6 +285,14 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
 
 extern int g_flags;
 
+struct IoBufs {
+  const double* a_src = nullptr;
+  long long lda = 0;
+  const int* arrive = nullptr;
+  double* r_dst = nullptr;
+  long long ldr = 0;
+};
+
 struct DevView {
   const Item* items;
   const int32_t* preds;
@@ -234,13 +303,13 @@ struct DevView {
 
 template <int NB, bool TRANST>
 cudaError_t launch_exec(const DevView& d, const double* vtiles, double* tiles, double* tg, double* te, int p,
-                        unsigned long long* trace, int grid, cudaStream_t st);
+                        unsigned long long* trace, int grid, cudaStream_t st, const IoBufs& io);
 
 // specializations live in tqr_exec_<nb><t|n>.cu
 #define TQR_DECLARE_LAUNCH(NB, TR)                                                                                  \
   template <>                                                                                                      \
   cudaError_t launch_exec<NB, TR>(const DevView& d, const double* vtiles, double* tiles, double* tg, double* te,  \
-                                  int p, unsigned long long* trace, int grid, cudaStream_t st);
+                                  int p, unsigned long long* trace, int grid, cudaStream_t st, const IoBufs& io);
 TQR_DECLARE_LAUNCH(64, true)
 TQR_DECLARE_LAUNCH(64, false)
 TQR_DECLARE_LAUNCH(256, true)
@@ -249,12 +318,14 @@ TQR_DECLARE_LAUNCH(256, false)
 #define TQR_DEFINE_LAUNCH(NB, TR)                                                                                   \
   template <>                                                                                                      \
   cudaError_t launch_exec<NB, TR>(const DevView& d, const double* vtiles, double* tiles, double* tg, double* te,  \
-                                  int p, unsigned long long* trace, int grid, cudaStream_t st) {                   \
+                                  int p, unsigned long long* trace, int grid, cudaStream_t st,                     \
+                                  const IoBufs& io) {                                                              \
     auto kern = exec_kernel<NB, TR>;                                                                               \
     const size_t smem = Smem<NB>::BYTES;                                                                           \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));            \
     if (e != cudaSuccess) return e;                                                                                \
-    ExecParams P{d.items, d.preds, d.n_items, d.done, d.queue, vtiles, tiles, tg, te, p, trace, g_flags};                   \
+    ExecParams P{d.items,  d.preds, d.n_items, d.done,  d.queue,  vtiles,   tiles, tg,                              \
+                 te,       p,       trace,     g_flags, io.a_src, io.lda, io.arrive, io.r_dst, io.ldr};             \
     kern<<<grid, NTP, smem, st>>>(P);                                                                               \
     return cudaGetLastError();                                                                                     \
   }

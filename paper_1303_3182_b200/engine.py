@@ -32,14 +32,20 @@ class Plan:
     """A QrBuild compiled into a static device schedule for tile size nb
     (tqr_plan_create).  Reusable across matrices of the same shape."""
 
-    def __init__(self, build: QrBuild, nb=256, ib=32):
+    IO_IN, IO_OUT = 1, 2
+
+    def __init__(self, build: QrBuild, nb=256, ib=32, io=0):
+        """io: 0 for device-resident input/output, or IO_IN | IO_OUT to
+        compile PACK / UNPACK work items that overlap the host transfers
+        with the factorization (factor_stream)."""
         if not torch.cuda.is_available():
             raise RuntimeError("tiled QR needs a CUDA device (no CPU fallback)")
         if build._h is None or not build.keep_trace:
             raise ValueError("the plan needs a QrBuild made with keep_trace=True")
         self.build = build
+        self.io = int(io)
         h = C.c_void_p()
-        check(lib().tqr_plan_create(build._h, int(nb), int(ib), C.byref(h)))
+        check(lib().tqr_plan_create_io(build._h, int(nb), int(ib), self.io, C.byref(h)))
         self._h = h
         info = _lib.PlanInfo()
         check(lib().tqr_plan_get_info(h, C.byref(info)))
@@ -72,6 +78,50 @@ class Plan:
 
     def factor(self, tiles, tg, te, stream=None):
         check(lib().tqr_factor(self._h, _vp(tiles), _vp(tg), _vp(te), _stream_ptr(stream)))
+
+    def factor_stream(self, A_host, R_host, tiles, tg, te, stage, flags, copy_stream):
+        """Host-to-host factorization with transfers overlapped: the tile
+        rows of the pinned row-major A_host are copied into `stage` on
+        `copy_stream`, each followed by a 4-byte arrival flag; PACK items
+        consume them as they land and UNPACK items write every finished R
+        tile straight into the pinned row-major R_host (zeros strictly below
+        the diagonal tiles must already be there).  Returns when R is done."""
+        assert self.io == (self.IO_IN | self.IO_OUT)
+        assert A_host.is_pinned() and R_host.is_pinned()
+        nb = self.nb
+        cs = torch.cuda.current_stream()
+        flags.zero_()
+        ready = torch.cuda.Event()
+        ready.record(cs)
+        if not hasattr(self, "_ones") or self._ones.numel() < self.p:
+            self._ones = torch.ones(self.p, dtype=torch.int32).pin_memory()
+        check(lib().tqr_factor_io(self._h, _vp(stage), stage.stride(0), _vp(flags), _vp(tiles), _vp(tg), _vp(te),
+                                  C.c_void_p(R_host.data_ptr()), R_host.stride(0), _stream_ptr(cs)))
+        copy_stream.wait_event(ready)
+        with torch.cuda.stream(copy_stream):
+            for i in self.arrival_order():
+                stage[i * nb:(i + 1) * nb].copy_(A_host[i * nb:(i + 1) * nb], non_blocking=True)
+                flags[i:i + 1].copy_(self._ones[i:i + 1], non_blocking=True)
+        cs.synchronize()
+
+    def arrival_order(self):
+        """Tile rows in the order the elimination list first pairs them in
+        column 1 (pivot, then target), so eliminations can start while the
+        matrix is still streaming in; unpaired rows last."""
+        if getattr(self, "_arrival", None) is None:
+            seen, order = set(), []
+            elim = self.build.elim
+            if elim is not None:
+                for e in elim:
+                    if e.k != 1:
+                        continue
+                    for r in (e.piv, e.i):
+                        if r not in seen:
+                            seen.add(r)
+                            order.append(r - 1)
+            order += [r for r in range(self.p) if r + 1 not in seen]
+            self._arrival = order
+        return self._arrival
 
     def apply_q(self, trans, tiles, tg, te, c_tiles, c_cols, stream=None):
         check(lib().tqr_apply_q(self._h, int(bool(trans)), _vp(tiles), _vp(tg), _vp(te), _vp(c_tiles),
@@ -123,6 +173,28 @@ class TiledQR:
         E = torch.zeros((P.m, P.n), dtype=torch.float64, device=self.tiles.device)
         E[:P.n].fill_diagonal_(1.0)
         return self.apply_q(E, trans=False)
+
+
+def tiled_qr_host(A_host, R_host=None, nb=256, algo="greedy", family="TT", bs=None, grasap_i=1, plan=None,
+                  buffers=None):
+    """Host matrix in, host R out, with the transfers overlapped with the
+    factorization (PACK/UNPACK work items).  A_host: pinned fp64 m x n
+    (row-major); returns (R_host, TiledQR)."""
+    A_host = A_host if A_host.is_pinned() else A_host.pin_memory()
+    m, n = A_host.shape
+    if plan is None:
+        build = build_tree(m // nb, n // nb, algo, family=family, bs=bs, grasap_i=grasap_i)
+        plan = Plan(build, nb, io=Plan.IO_IN | Plan.IO_OUT)
+    if R_host is None:
+        R_host = torch.zeros((n, n), dtype=torch.float64).pin_memory()
+    if buffers is None:
+        tiles, tg, te = plan.alloc()
+        stage = torch.empty((m, n), dtype=torch.float64, device=tiles.device)
+        flags = torch.zeros(plan.p, dtype=torch.int32, device=tiles.device)
+        buffers = (tiles, tg, te, stage, flags, torch.cuda.Stream())
+    tiles, tg, te, stage, flags, cstream = buffers
+    plan.factor_stream(A_host, R_host, tiles, tg, te, stage, flags, cstream)
+    return R_host, TiledQR(plan, tiles, tg, te)
 
 
 def tiled_qr(A, nb=256, ib=32, algo="greedy", family="TT", bs=None, grasap_i=1, elim=None, plan=None):

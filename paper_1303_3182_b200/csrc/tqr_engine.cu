@@ -178,14 +178,22 @@ void expand(const std::vector<Task>& tasks, const std::vector<std::vector<int32_
 }
 
 // Device-realistic relative cost of one work item (an update slab = 1).
+// Overridable for tuning: TQR_COST_PANEL (GEQRT/TTQRT at nb=256),
+// TQR_COST_PACK, TQR_COST_UNPACK.
+double env_cost(const char* k, double dflt) {
+  const char* v = getenv(k);
+  return v ? atof(v) : dflt;
+}
 inline double item_cost(int kind, int nb) {
+  static const double panel = env_cost("TQR_COST_PANEL", 3.5), pack = env_cost("TQR_COST_PACK", 0.1),
+                      unpack = env_cost("TQR_COST_UNPACK", 0.5);
   const double big = nb >= 256 ? 1.0 : 0.5;
   switch (kind) {
-    case tqr::PACK: return 0.1;
-    case tqr::UNPACK: return 0.5;
-    case tqr::GEQRT: return 3.0 * big + 0.5;
-    case tqr::TTQRT: return 2.5 * big + 0.5;
-    case tqr::TSQRT: return 4.0 * big + 0.5;
+    case tqr::PACK: return pack;
+    case tqr::UNPACK: return unpack;
+    case tqr::GEQRT: return (panel - 0.5) * big + 0.5;
+    case tqr::TTQRT: return (panel - 1.0) * big + 0.5;
+    case tqr::TSQRT: return (panel + 0.5) * big + 0.5;
     case tqr::TSMQR: return 2.0;
     default: return 1.0;
   }
@@ -196,7 +204,8 @@ inline double item_cost(int kind, int nb) {
 // taskgraph.py:338-362) and lowest-id tie break, the MaxCP policy of the
 // reference's list scheduler (sched.py:77-156).  The result is a
 // topological order, which the executor's deadlock-freedom needs.
-void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers, int nb) {
+void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers, int nb,
+              const std::vector<double>& col_release = {}) {
   const size_t n = items.size();
   if (n == 0) return;
   std::vector<int32_t> nsucc(n + 1, 0);
@@ -216,21 +225,40 @@ void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers
     double best = 0.0;
     for (int32_t k = nsucc[v]; k < nsucc[v + 1]; ++k) best = std::max(best, prio[size_t(succ[size_t(k)])]);
     prio[v] = w[v] + best;
-    if (items[v].kind == tqr::UNPACK) prio[v] = 1e12;  // ship finished R tiles at once
   }
+  // ship finished R tiles at once (after the pass, so that their
+  // predecessors keep plain critical-path priorities)
+  for (size_t v = 0; v < n; ++v)
+    if (items[v].kind == tqr::UNPACK) prio[v] = 1e12;
   std::vector<int32_t> indeg(n);
   for (size_t v = 0; v < n; ++v) indeg[v] = items[v].pred_n;
+  // PACK(i,j) cannot start before tile column j has arrived (col_release[j-1])
+  auto release = [&](size_t v) {
+    return items[v].kind == tqr::PACK && !col_release.empty() ? col_release[size_t(items[v].j - 1)] : 0.0;
+  };
   using RQ = std::pair<double, int32_t>;  // (-priority, id) min-heap == max priority, lowest id
   std::priority_queue<RQ, std::vector<RQ>, std::greater<RQ>> ready;
+  using EV = std::pair<double, int32_t>;  // (time, id)
+  std::priority_queue<EV, std::vector<EV>, std::greater<EV>> pending;  // dependency-free, not yet released
+  auto make_ready = [&](size_t v, double now) {
+    const double r = release(v);
+    if (r > now)
+      pending.emplace(r, int32_t(v));
+    else
+      ready.emplace(-prio[v], int32_t(v));
+  };
   for (size_t v = 0; v < n; ++v)
-    if (indeg[v] == 0) ready.emplace(-prio[v], int32_t(v));
-  using EV = std::pair<double, int32_t>;  // (finish time, id)
+    if (indeg[v] == 0) make_ready(v, 0.0);
   std::priority_queue<EV, std::vector<EV>, std::greater<EV>> running;
   std::vector<int32_t> order;
   order.reserve(n);
   double now = 0.0;
   int idle = workers;
   while (order.size() < n) {
+    while (!pending.empty() && pending.top().first <= now) {
+      ready.emplace(-prio[size_t(pending.top().second)], pending.top().second);
+      pending.pop();
+    }
     while (idle > 0 && !ready.empty()) {
       const int32_t v = ready.top().second;
       ready.pop();
@@ -238,15 +266,17 @@ void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers
       running.emplace(now + w[size_t(v)], v);
       --idle;
     }
-    if (running.empty()) break;  // cannot happen for a DAG
-    now = running.top().first;
+    if (running.empty() && pending.empty()) break;  // cannot happen for a DAG
+    double next = running.empty() ? pending.top().first : running.top().first;
+    if (!pending.empty() && idle > 0) next = std::min(next, pending.top().first);
+    now = std::max(now, next);
     while (!running.empty() && running.top().first <= now) {
       const int32_t u = running.top().second;
       running.pop();
       ++idle;
       for (int32_t k = nsucc[size_t(u)]; k < nsucc[size_t(u) + 1]; ++k) {
         const int32_t v = succ[size_t(k)];
-        if (--indeg[size_t(v)] == 0) ready.emplace(-prio[size_t(v)], v);
+        if (--indeg[size_t(v)] == 0) make_ready(size_t(v), now);
       }
     }
   }
@@ -288,6 +318,7 @@ struct tqr_plan {
   int64_t n_tasks = 0;
   double flops = 0;
   std::vector<Task> trace;  // factorization trace (for apply-Q)
+  std::vector<int32_t> arrival;  // io & 1: tile columns (1-based) in host transfer order
   DevSched fac;
   std::map<std::pair<int, int>, DevSched> aq;  // (trans, c_cols) -> apply-Q schedule
   ~tqr_plan() {
@@ -298,7 +329,35 @@ struct tqr_plan {
 
 namespace {
 
-unsigned long long* g_trace = nullptr;  // tqr_set_trace: per-item timestamps of the next run
+unsigned long long* g_trace = nullptr;
+
+// CUDA stream memory operations (driver API, resolved at run time so the
+// library needs no libcuda link): a copy stream raises / waits on 32-bit
+// flags in device memory that the running executor polls / bumps.
+using WriteV32 = int (*)(void*, unsigned long long, unsigned, unsigned);
+using WaitV32 = int (*)(void*, unsigned long long, unsigned, unsigned);
+WriteV32 g_wv32 = nullptr;
+WaitV32 g_wt32 = nullptr;
+bool stream_memops() {
+  static int ok = -1;
+  if (ok < 0) {
+    void* f1 = nullptr;
+    void* f2 = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    ok = cudaGetDriverEntryPoint("cuStreamWriteValue32", &f1, cudaEnableDefault, &q1) == cudaSuccess &&
+         cudaGetDriverEntryPoint("cuStreamWaitValue32", &f2, cudaEnableDefault, &q2) == cudaSuccess &&
+         q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && f1 && f2;
+    g_wv32 = reinterpret_cast<WriteV32>(f1);
+    g_wt32 = reinterpret_cast<WaitV32>(f2);
+  }
+  return ok == 1;
+}
+int g_write32(cudaStream_t s, int* addr, unsigned v) {  // CU_STREAM_WRITE_VALUE_DEFAULT
+  return g_wv32(s, reinterpret_cast<unsigned long long>(addr), v, 0);
+}
+int g_wait32(cudaStream_t s, int* addr, unsigned v) {  // CU_STREAM_WAIT_VALUE_GEQ
+  return g_wt32(s, reinterpret_cast<unsigned long long>(addr), v, 0);
+}  // tqr_set_trace: per-item timestamps of the next run
 
 // debug knobs from the environment: TQR_GRID (CTAs), TQR_FLAGS (bit 0: no early staging)
 int env_int(const char* k, int dflt) {
@@ -391,6 +450,18 @@ int tqr_plan_create_io(const tqr_build* hb, int nb, int ib, int io, tqr_plan** o
             recs.push_back({tqr::UNPACK, i, j, -1, -1, 0});
             tasks.push_back({tqr::UNPACK, i, -1, -1, j});
           }
+      // host transfer order: tile columns left to right (the order the
+      // factorization consumes them; a column block is one 2D copy at full
+      // link rate), PACK(i,j) released when column j has landed
+      std::vector<double> col_release;
+      if (io & 1) {
+        for (int j = 1; j <= b.q; ++j) P->arrival.push_back(j);
+        // modeled arrival in item-cost units: one nb-column block of the m
+        // rows at ~50 GB/s host link; an update slab item ~ 54 us at nb=256
+        const double unit_s = 54e-6 * (double(nb) / 256.0) * (double(nb) / 256.0);
+        const double col_s = double(nb) * double(b.p) * nb * 8.0 / 50e9;
+        for (int j = 1; j <= b.q; ++j) col_release.push_back(double(j) * col_s / unit_s);
+      }
       const size_t m = tasks.size();
       // hazard edges of the reference model, weighted ASAP order (QR weights)
       auto edges = tqr::hazard_edges(b.p, b.q, recs);
@@ -406,7 +477,7 @@ int tqr_plan_create_io(const tqr_build* hb, int nb, int ib, int io, tqr_plan** o
       std::vector<Item> items;
       std::vector<int32_t> preds;
       expand(tasks, in, order, nb / WS, items, preds);
-      cp_order(items, preds, num_sms_host(), nb);
+      cp_order(items, preds, num_sms_host(), nb, col_release);
       upload(P->fac, items, preds);
       const double mm = double(b.p) * nb, nn = double(b.q) * nb;
       P->flops = 2.0 * nn * nn * (mm - nn / 3.0);
@@ -448,15 +519,108 @@ int tqr_factor(tqr_plan* P, double* tiles, double* tg, double* te, void* stream)
 }
 
 int tqr_factor_io(tqr_plan* P, const double* a_src, int64_t lda, const int* arrive, double* tiles, double* tg,
-                  double* te, double* r_dst, int64_t ldr, void* stream) {
+                  double* te, double* r_dst, int64_t ldr, int* r_ready, void* stream) {
   int rc = tqr::guard([&] {
     if (!P) throw tqr::ValueError("null plan");
     if ((P->io & 1) && (!a_src || !arrive)) throw tqr::ValueError("plan streams its input: a_src and arrive needed");
     if ((P->io & 2) && !r_dst) throw tqr::ValueError("plan streams R out: r_dst needed");
   });
   if (rc) return rc;
-  IoBufs io{a_src, lda, arrive, r_dst, ldr};
+  IoBufs io{a_src, lda, arrive, r_dst, ldr, r_ready};
   return cuda_guarded(run(P->fac, P->nb, true, tiles, tiles, tg, te, P->p, static_cast<cudaStream_t>(stream), io));
+}
+
+int tqr_plan_arrival_order(const tqr_plan* P, int32_t* cols_out) {
+  return tqr::guard([&] {
+    if (!P) throw tqr::ValueError("null plan");
+    if (!(P->io & 1)) throw tqr::ValueError("plan does not stream its input");
+    std::copy(P->arrival.begin(), P->arrival.end(), cols_out);
+  });
+}
+
+int tqr_qr_host(tqr_plan* P, const double* a_host, int64_t lda_h, double* r_host, int64_t ldr_h, double* stage,
+                int* arrive, double* tiles, double* tg, double* te, double* r_dev, int* r_ready, void* stream,
+                void* copy_in, void* copy_out) {
+  int rc = tqr::guard([&] {
+    if (!P) throw tqr::ValueError("null plan");
+    if (P->io != 3) throw tqr::ValueError("tqr_qr_host needs a plan made with io = 3");
+    if (!a_host || !r_host || !stage || !arrive || !r_dev || !r_ready)
+      throw tqr::ValueError("null buffer");
+    if (!stream_memops()) throw std::runtime_error("CUDA stream memory operations unavailable");
+  });
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream), ci = static_cast<cudaStream_t>(copy_in),
+               co = static_cast<cudaStream_t>(copy_out);
+  const int nb = P->nb, q = P->q;
+  const int64_t n = int64_t(q) * nb;
+  cudaError_t e;
+  auto ck = [&](cudaError_t x) { return x == cudaSuccess ? (e = x, false) : (e = x, true); };
+  auto cu = [&](int r) { return r == 0 ? (e = cudaSuccess, false) : (e = cudaErrorUnknown, true); };
+  cudaEvent_t ev0, ev1, ev2;
+  if (ck(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming))) return cuda_guarded(e);
+  cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ev2, cudaEventDisableTiming);
+  // TQR_IO_DEBUG: print kernel / input / output completion times (ms)
+  const bool dbg = env_int("TQR_IO_DEBUG", 0) != 0;
+  cudaEvent_t d0 = nullptr, dk = nullptr, di = nullptr, dout = nullptr;
+  if (dbg) {
+    cudaEventCreate(&d0);
+    cudaEventCreate(&dk);
+    cudaEventCreate(&di);
+    cudaEventCreate(&dout);
+    cudaEventRecord(d0, st);
+  }
+  do {
+    if (ck(cudaMemsetAsync(arrive, 0, size_t(q) * sizeof(int), st))) break;
+    if (ck(cudaMemsetAsync(r_ready, 0, size_t(q) * sizeof(int), st))) break;
+    if (ck(cudaEventRecord(ev0, st))) break;
+    if (ck(cudaStreamWaitEvent(ci, ev0, 0)) || ck(cudaStreamWaitEvent(co, ev0, 0))) break;
+    IoBufs io{stage, n, arrive, r_dev, n, r_ready};
+    if (ck(run(P->fac, nb, true, tiles, tiles, tg, te, P->p, st, io))) break;
+    if (dbg) cudaEventRecord(dk, st);
+    bool bad = false;
+    // input: one nb-column block (m rows) per arrival, then raise its flag
+    // (the write value is ordered after the copy on the copy stream)
+    const size_t m = size_t(P->p) * nb;
+    for (int c : P->arrival) {
+      const size_t off = size_t(c - 1) * nb;
+      if ((bad = ck(cudaMemcpy2DAsync(stage + off, size_t(n) * 8, a_host + off, size_t(lda_h) * 8, size_t(nb) * 8, m,
+                                      cudaMemcpyHostToDevice, ci))))
+        break;
+      if ((bad = cu(g_write32(ci, arrive + (c - 1), 1)))) break;
+    }
+    if (bad) break;
+    // output: tile row i of R once its q-i+1 tiles are written out
+    for (int i = 1; i <= q && !bad; ++i) {
+      if ((bad = cu(g_wait32(co, r_ready + (i - 1), unsigned(q - i + 1))))) break;
+      const size_t r0 = size_t(i - 1) * nb;
+      bad = ck(cudaMemcpy2DAsync(r_host + r0 * size_t(ldr_h) + r0, size_t(ldr_h) * 8, r_dev + r0 * size_t(n) + r0,
+                                 size_t(n) * 8, size_t(n - int64_t(r0)) * 8, size_t(nb), cudaMemcpyDeviceToHost, co));
+    }
+    if (bad) break;
+    if (dbg) {
+      cudaEventRecord(di, ci);
+      cudaEventRecord(dout, co);
+    }
+    if (ck(cudaEventRecord(ev1, ci)) || ck(cudaEventRecord(ev2, co))) break;
+    if (ck(cudaStreamWaitEvent(st, ev1, 0)) || ck(cudaStreamWaitEvent(st, ev2, 0))) break;
+  } while (false);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  cudaEventDestroy(ev2);
+  if (dbg) {
+    cudaStreamSynchronize(st);
+    float a = 0, b2 = 0, c = 0;
+    cudaEventElapsedTime(&a, d0, dk);
+    cudaEventElapsedTime(&b2, d0, di);
+    cudaEventElapsedTime(&c, d0, dout);
+    fprintf(stderr, "tqr_qr_host: kernel %.2f ms, input %.2f ms, output %.2f ms\n", a, b2, c);
+    cudaEventDestroy(d0);
+    cudaEventDestroy(dk);
+    cudaEventDestroy(di);
+    cudaEventDestroy(dout);
+  }
+  return cuda_guarded(e);
 }
 
 int tqr_apply_q(tqr_plan* P, int trans, const double* tiles, const double* tg, const double* te, double* c_tiles,

@@ -35,9 +35,10 @@ struct ExecParams {
   // streaming I/O (PACK / UNPACK items)
   const double* a_src;  // row-major input staging (device), ld lda
   long long lda;
-  const int* arrive;  // per tile row: nonzero once its rows landed in a_src
-  double* r_dst;      // row-major R output (host-mapped pinned memory), ld ldr
+  const int* arrive;  // per tile column: nonzero once its columns landed in a_src
+  double* r_dst;      // row-major R output (device-accessible), ld ldr
   long long ldr;
+  int* r_ready;  // optional: per tile row of R, count of tiles written out
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -91,46 +92,79 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
   return v;
 }
 
-// PACK(i,j): wait until tile row i of the row-major input has landed (the
-// host's flag copy follows the row block on the same copy stream), then
-// transpose tile (i,j) into the tile-major, column-major-tile layout.
+// PACK(i,j): wait until tile column j of the row-major input has landed (the
+// host's copy stream raises arrive[j-1] after the column block), then transpose
+// tile (i,j) into the tile-major, column-major-tile layout.  32-row chunks
+// through padded smem (LD = NB+1: both phases bank-conflict free); the next
+// chunk's loads are issued before the current chunk is written out.
 template <int NB>
 __device__ void pack_item(double* sm, const ExecParams& P, int i, int j, int tid) {
+  constexpr int CR = 32, LD = NB + 1, PER = CR * NB / NT;
   if (tid == 0) {
-    while (ld_acquire_sys(P.arrive + (i - 1)) == 0) __nanosleep(200);
+    while (ld_acquire_sys(P.arrive + (j - 1)) == 0) __nanosleep(256);
   }
   csync();
   double* dst = P.tiles + toff<NB>(P.p, i, j);
   const double* src = P.a_src + (long long)(i - 1) * NB * P.lda + (long long)(j - 1) * NB;
-  double(*t)[33] = reinterpret_cast<double(*)[33]>(sm);  // 32 x 33 transpose tile
   const int warp = tid >> 5, lane = tid & 31;
-  for (int s = 0; s < (NB / 32) * (NB / 32); ++s) {
-    const int ra = (s % (NB / 32)) * 32, cb = (s / (NB / 32)) * 32;
-    for (int y = warp; y < 32; y += NW) t[y][lane] = __ldcg(src + (long long)(ra + y) * P.lda + cb + lane);
+  double v[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int e = tid + u * NT;
+    v[u] = __ldcg(src + (long long)(e / NB) * P.lda + e % NB);
+  }
+  for (int r0 = 0; r0 < NB; r0 += CR) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + u * NT;
+      sm[(e / NB) * LD + e % NB] = v[u];
+    }
     csync();
-    for (int y = warp; y < 32; y += NW) dst[(ra + lane) + size_t(cb + y) * NB] = t[lane][y];
+    if (r0 + CR < NB) {
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int e = tid + u * NT;
+        v[u] = __ldcg(src + (long long)(r0 + CR + e / NB) * P.lda + e % NB);
+      }
+    }
+#pragma unroll 8
+    for (int c = warp; c < NB; c += NW) __stcg(dst + size_t(c) * NB + r0 + lane, sm[lane * LD + c]);
     csync();
   }
 }
 
-// UNPACK(i,j): final R tile (i,j) (j >= i) -> row-major R in host-mapped
-// memory (upper triangle for the diagonal tile, zeros below it).
+// UNPACK(i,j): final R tile (i,j) (j >= i) -> row-major R (upper triangle
+// for the diagonal tile, zeros below it); then, if the caller asked for it,
+// count the tile in r_ready[i-1] so a copy stream waiting on that counter
+// can ship R's tile row i as soon as all q-i+1 of its tiles are out.
 template <int NB>
 __device__ void unpack_item(double* sm, const ExecParams& P, int i, int j, int tid) {
+  constexpr int CR = 32, LD = NB + 1, PER = CR * NB / NT;
   const double* src = P.tiles + toff<NB>(P.p, i, j);
   double* dst = P.r_dst + (long long)(i - 1) * NB * P.ldr + (long long)(j - 1) * NB;
-  double(*t)[33] = reinterpret_cast<double(*)[33]>(sm);
   const int warp = tid >> 5, lane = tid & 31;
-  for (int s = 0; s < (NB / 32) * (NB / 32); ++s) {
-    const int ra = (s % (NB / 32)) * 32, cb = (s / (NB / 32)) * 32;
-    for (int y = warp; y < 32; y += NW) {
-      double v = __ldcg(src + (ra + lane) + size_t(cb + y) * NB);  // (row ra+lane, col cb+y)
-      if (i == j && ra + lane > cb + y) v = 0.0;
-      t[y][lane] = v;
+  for (int r0 = 0; r0 < NB; r0 += CR) {
+    double v[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int c = warp + u * NW;
+      v[u] = __ldcg(src + size_t(c) * NB + r0 + lane);
+      if (i == j && r0 + lane > c) v[u] = 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) sm[lane * LD + warp + u * NW] = v[u];
+    csync();
+#pragma unroll 8
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + u * NT;
+      __stcg(dst + (long long)(r0 + e / NB) * P.ldr + e % NB, sm[(e / NB) * LD + e % NB]);
     }
     csync();
-    for (int y = warp; y < 32; y += NW) dst[(long long)(ra + y) * P.ldr + cb + lane] = t[lane][y];
+  }
+  if (P.r_ready) {
+    __threadfence_system();
     csync();
+    if (tid == 0) atomicAdd(P.r_ready + (i - 1), 1);
   }
 }
 
@@ -291,6 +325,7 @@ struct IoBufs {
   const int* arrive = nullptr;
   double* r_dst = nullptr;
   long long ldr = 0;
+  int* r_ready = nullptr;
 };
 
 struct DevView {
@@ -325,7 +360,7 @@ TQR_DECLARE_LAUNCH(256, false)
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));            \
     if (e != cudaSuccess) return e;                                                                                \
     ExecParams P{d.items,  d.preds, d.n_items, d.done,  d.queue,  vtiles,   tiles, tg,                              \
-                 te,       p,       trace,     g_flags, io.a_src, io.lda, io.arrive, io.r_dst, io.ldr};             \
+                 te,       p,       trace,     g_flags, io.a_src, io.lda, io.arrive, io.r_dst, io.ldr, io.r_ready};           \
     kern<<<grid, NTP, smem, st>>>(P);                                                                               \
     return cudaGetLastError();                                                                                     \
   }

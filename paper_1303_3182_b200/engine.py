@@ -11,6 +11,7 @@ the library this module raises.
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 
 import torch
 
@@ -79,49 +80,42 @@ class Plan:
     def factor(self, tiles, tg, te, stream=None):
         check(lib().tqr_factor(self._h, _vp(tiles), _vp(tg), _vp(te), _stream_ptr(stream)))
 
-    def factor_stream(self, A_host, R_host, tiles, tg, te, stage, flags, copy_stream):
-        """Host-to-host factorization with transfers overlapped: the tile
-        rows of the pinned row-major A_host are copied into `stage` on
-        `copy_stream`, each followed by a 4-byte arrival flag; PACK items
-        consume them as they land and UNPACK items write every finished R
-        tile straight into the pinned row-major R_host (zeros strictly below
-        the diagonal tiles must already be there).  Returns when R is done."""
+    def factor_stream(self, A_host, R_host, bufs):
+        """Host-to-host factorization with every transfer overlapped
+        (tqr_qr_host): the nb-column blocks of the pinned row-major A_host
+        go up in arrival_order() on one copy stream, PACK items consume them as
+        they land, UNPACK items write finished R tiles to a device R and a
+        second copy stream ships each tile row of R into the pinned R_host
+        as soon as it is complete (zeros strictly below the diagonal tiles
+        must already be there).  Returns when R_host is filled."""
         assert self.io == (self.IO_IN | self.IO_OUT)
         assert A_host.is_pinned() and R_host.is_pinned()
-        nb = self.nb
+        assert A_host.shape == (self.m, self.n) and R_host.shape == (self.n, self.n)
         cs = torch.cuda.current_stream()
-        flags.zero_()
-        ready = torch.cuda.Event()
-        ready.record(cs)
-        if not hasattr(self, "_ones") or self._ones.numel() < self.p:
-            self._ones = torch.ones(self.p, dtype=torch.int32).pin_memory()
-        check(lib().tqr_factor_io(self._h, _vp(stage), stage.stride(0), _vp(flags), _vp(tiles), _vp(tg), _vp(te),
-                                  C.c_void_p(R_host.data_ptr()), R_host.stride(0), _stream_ptr(cs)))
-        copy_stream.wait_event(ready)
-        with torch.cuda.stream(copy_stream):
-            for i in self.arrival_order():
-                stage[i * nb:(i + 1) * nb].copy_(A_host[i * nb:(i + 1) * nb], non_blocking=True)
-                flags[i:i + 1].copy_(self._ones[i:i + 1], non_blocking=True)
+        check(lib().tqr_qr_host(self._h, C.c_void_p(A_host.data_ptr()), A_host.stride(0),
+                                C.c_void_p(R_host.data_ptr()), R_host.stride(0), _vp(bufs.stage), _vp(bufs.arrive),
+                                _vp(bufs.tiles), _vp(bufs.tg), _vp(bufs.te), _vp(bufs.r_dev), _vp(bufs.r_ready),
+                                _stream_ptr(cs), _stream_ptr(bufs.copy_in), _stream_ptr(bufs.copy_out)))
         cs.synchronize()
 
+    def stream_buffers(self, device=None):
+        """Device scratch for factor_stream (reusable across calls)."""
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        tiles, tg, te = self.alloc(dev)
+        return StreamBuffers(tiles, tg, te, torch.empty((self.m, self.n), dtype=torch.float64, device=dev),
+                             torch.zeros(self.q, dtype=torch.int32, device=dev),
+                             torch.empty((self.n, self.n), dtype=torch.float64, device=dev),
+                             torch.zeros(self.q, dtype=torch.int32, device=dev),
+                             torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+
     def arrival_order(self):
-        """Tile rows in the order the elimination list first pairs them in
-        column 1 (pivot, then target), so eliminations can start while the
-        matrix is still streaming in; unpaired rows last."""
-        if getattr(self, "_arrival", None) is None:
-            seen, order = set(), []
-            elim = self.build.elim
-            if elim is not None:
-                for e in elim:
-                    if e.k != 1:
-                        continue
-                    for r in (e.piv, e.i):
-                        if r not in seen:
-                            seen.add(r)
-                            order.append(r - 1)
-            order += [r for r in range(self.p) if r + 1 not in seen]
-            self._arrival = order
-        return self._arrival
+        """1-based tile columns in host transfer order
+        (tqr_plan_arrival_order): left to right, as the factorization
+        consumes them."""
+        import numpy as np
+        out = np.empty(self.q, dtype=np.int32)
+        check(lib().tqr_plan_arrival_order(self._h, _lib.ptr_i32(out)))
+        return out.tolist()
 
     def apply_q(self, trans, tiles, tg, te, c_tiles, c_cols, stream=None):
         check(lib().tqr_apply_q(self._h, int(bool(trans)), _vp(tiles), _vp(tg), _vp(te), _vp(c_tiles),
@@ -143,6 +137,19 @@ class Plan:
         A = A.contiguous()
         check(lib().tqr_pack(_vp(A), A.stride(0), 1, _vp(tiles), self.p, cols, self.nb, _stream_ptr(stream)))
         return tiles
+
+
+@dataclasses.dataclass
+class StreamBuffers:
+    tiles: torch.Tensor
+    tg: torch.Tensor
+    te: torch.Tensor
+    stage: torch.Tensor
+    arrive: torch.Tensor
+    r_dev: torch.Tensor
+    r_ready: torch.Tensor
+    copy_in: torch.cuda.Stream
+    copy_out: torch.cuda.Stream
 
 
 class TiledQR:
@@ -178,9 +185,10 @@ class TiledQR:
 def tiled_qr_host(A_host, R_host=None, nb=256, algo="greedy", family="TT", bs=None, grasap_i=1, plan=None,
                   buffers=None):
     """Host matrix in, host R out, with the transfers overlapped with the
-    factorization (PACK/UNPACK work items).  A_host: pinned fp64 m x n
-    (row-major); returns (R_host, TiledQR)."""
-    A_host = A_host if A_host.is_pinned() else A_host.pin_memory()
+    factorization (PACK/UNPACK work items, tqr_qr_host).  A_host: fp64
+    m x n row-major (pinned for full overlap); returns (R_host, TiledQR)."""
+    A_host = torch.as_tensor(A_host, dtype=torch.float64)
+    A_host = A_host if A_host.is_pinned() else A_host.contiguous().pin_memory()
     m, n = A_host.shape
     if plan is None:
         build = build_tree(m // nb, n // nb, algo, family=family, bs=bs, grasap_i=grasap_i)
@@ -188,13 +196,9 @@ def tiled_qr_host(A_host, R_host=None, nb=256, algo="greedy", family="TT", bs=No
     if R_host is None:
         R_host = torch.zeros((n, n), dtype=torch.float64).pin_memory()
     if buffers is None:
-        tiles, tg, te = plan.alloc()
-        stage = torch.empty((m, n), dtype=torch.float64, device=tiles.device)
-        flags = torch.zeros(plan.p, dtype=torch.int32, device=tiles.device)
-        buffers = (tiles, tg, te, stage, flags, torch.cuda.Stream())
-    tiles, tg, te, stage, flags, cstream = buffers
-    plan.factor_stream(A_host, R_host, tiles, tg, te, stage, flags, cstream)
-    return R_host, TiledQR(plan, tiles, tg, te)
+        buffers = plan.stream_buffers()
+    plan.factor_stream(A_host, R_host, buffers)
+    return R_host, TiledQR(plan, buffers.tiles, buffers.tg, buffers.te)
 
 
 def tiled_qr(A, nb=256, ib=32, algo="greedy", family="TT", bs=None, grasap_i=1, elim=None, plan=None):

@@ -207,3 +207,12 @@ def test_streaming_io_matches_device_path(p, q, nb, algo):
     R_dev = tiled_qr(A, nb=nb, algo=algo).R().cpu()
     R_host, _ = tiled_qr_host(torch.from_numpy(A), nb=nb, algo=algo)
     assert torch.equal(R_host, R_dev)
+
+
+@pytest.mark.gpu
+def test_arrival_order_is_left_to_right_columns():
+    """tqr_qr_host ships tile columns left to right (the order the
+    factorization consumes them)."""
+    _need_gpu()
+    plan = Plan(P.build_tree(8, 4, "greedy"), 64, io=Plan.IO_IN | Plan.IO_OUT)
+    assert plan.arrival_order() == [1, 2, 3, 4]

@@ -18,7 +18,7 @@ import paper_1303_3182_b200 as P  # noqa: E402
 from paper_1303_3182_b200 import _lib  # noqa: E402
 from paper_1303_3182_b200.engine import Plan  # noqa: E402
 
-KIND = ["GEQRT", "TTQRT", "TSQRT", "UNMQR", "TTMQR", "TSMQR"]
+KIND = ["GEQRT", "TTQRT", "TSQRT", "UNMQR", "TTMQR", "TSMQR", "PACK", "UNPACK"]
 
 
 def main():
@@ -26,24 +26,42 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--out", default="gpurun_out/item_trace.json")
     ap.add_argument("--gantt", default=None)
+    ap.add_argument("--stream", action="store_true", help="trace the streaming host-to-host path")
     a = ap.parse_args()
     cfg = bench.CONFIGS[a.config]
     nb = cfg["nb"]
     p, q = cfg["m"] // nb, cfg["n"] // nb
     b = P.build_tree(p, q, cfg["algo"], family=cfg["family"])
-    plan = Plan(b, nb)
-    A = torch.from_numpy(bench.make_matrix(cfg)).cuda()
+    plan = Plan(b, nb, io=(Plan.IO_IN | Plan.IO_OUT) if a.stream else 0)
+    A = torch.from_numpy(bench.make_matrix(cfg))
     tiles, tg, te = plan.alloc()
+    if a.stream:
+        A = A.pin_memory()
+        R = torch.zeros((plan.n, plan.n), dtype=torch.float64).pin_memory()
+        bufs = plan.stream_buffers()
+        tiles, tg, te = bufs.tiles, bufs.tg, bufs.te
+        run = lambda: plan.factor_stream(A, R, bufs)  # noqa: E731
+        # raw pinned H2D bandwidth for reference
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        bufs.stage.copy_(A, non_blocking=True)
+        ev[1].record()
+        torch.cuda.synchronize()
+        h2d_ms = ev[0].elapsed_time(ev[1])
+    else:
+        A = A.cuda()
+        run = lambda: (plan.pack(A, tiles), plan.factor(tiles, tg, te))  # noqa: E731
     for _ in range(2):
-        plan.pack(A, tiles)
-        plan.factor(tiles, tg, te)
+        run()
+    torch.cuda.synchronize()
     n = plan.info.n_items
     tr = torch.zeros(4 * n + 64, dtype=torch.int64, device="cuda")
     _lib.lib().tqr_set_trace(C.c_void_p(tr.data_ptr()))
-    plan.pack(A, tiles)
+    import time
+    t_w = time.perf_counter()
+    run()
     torch.cuda.synchronize()
-    plan.factor(tiles, tg, te)
-    torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - t_w) * 1e3
     _lib.lib().tqr_set_trace(None)
     trc = tr.cpu().numpy()
     t = trc[:4 * n].reshape(n, 4)
@@ -55,7 +73,33 @@ def main():
     total = end.max()
     out = {"config": a.config, "items": int(n), "makespan_us": float(total),
            "gflops": plan.flops / (total * 1e-6) / 1e9, "per_kind": {}}
-    for kd in range(6):
+    if a.stream:
+        out["wall_ms"] = wall_ms
+        out["h2d_full_ms"] = h2d_ms
+        pk = items[:, 0] == 6
+        upk = items[:, 0] == 7
+        out["pack_last_ready_us"] = float(rdy[pk].max())
+        out["pack_ready_deciles_us"] = [round(float(x), 1) for x in np.percentile(rdy[pk], np.arange(0, 101, 10))]
+        cmp_ = ~(pk | upk)
+        out["compute_first_start_us"] = float(rdy[cmp_].min())
+        out["compute_last_end_us"] = float(end[cmp_].max())
+        out["unpack_last_end_us"] = float(end[upk].max())
+        # completion time of each tile row of R and the modeled D2H queue
+        rows_done = np.zeros(plan.q)
+        for r in np.nonzero(upk)[0]:
+            ii = items[r, 2] - 1
+            rows_done[ii] = max(rows_done[ii], end[r])
+        fin = 0.0
+        for ii in range(plan.q):
+            fin = max(fin, rows_done[ii]) + (plan.q - ii) * nb * nb * 8 / 50e9 * 1e6
+        out["r_rows_done_us"] = [round(float(x)) for x in rows_done]
+        out["modeled_copy_out_end_us"] = fin
+        # SM busy (compute kinds only) in 5% bins
+        bins = np.linspace(0, end.max(), 21)
+        out["compute_busy_by_5pct"] = [round(float(np.clip(np.minimum(end[cmp_], hi) - np.maximum(rdy[cmp_], lo), 0,
+                                                           None).sum() / ((hi - lo) * (int(sm.max()) + 1))), 3)
+                                       for lo, hi in zip(bins[:-1], bins[1:])]
+    for kd in range(8):
         msk = items[:, 0] == kd
         if not msk.any():
             continue

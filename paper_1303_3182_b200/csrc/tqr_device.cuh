@@ -19,6 +19,7 @@
 // (V as K x N and V^T) bank-conflict free.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 namespace tqrk {
 
@@ -129,7 +130,9 @@ struct NoPf {
 // 0 unit-lower (GE), 1 upper (TT), 2 full (TS).  V is staged already
 // masked; 8x8 sub-blocks that are structurally zero are skipped in both
 // GEMMs.
-template <int NB, bool TRANST, int TRI = 2, class PF = NoPf>
+// [RBL, RBH): compile-time bound on the row blocks this instance may touch,
+// so that x registers outside it can be in flight (loads) meanwhile.
+template <int NB, bool TRANST, int TRI = 2, int RBL = 0, int RBH = NB / IB, class PF = NoPf>
 __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int rb1, const double* __restrict__ Vs,
                                            const double* __restrict__ Ts, double* top, int lane,
                                            const double* top_s = nullptr, int drb = -1, PF pf = PF()) {
@@ -150,6 +153,7 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
       ap[nb][1] = v.y;
     }
   }
+  UPROF_DECL_V(_tq);
   // accumulate V^T X from zero and add the pivot rows once afterwards, as
   // LAPACK's dlarfb does (one rounding of the large operand per block)
 #pragma unroll
@@ -158,7 +162,7 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
   // row group are loaded while the current group's DMMAs issue
 #pragma unroll
   for (int rb = 0; rb < NB / IB; ++rb) {
-    if (rb >= rb0 && rb < rb1) {
+    if (rb >= RBL && rb < RBH && rb >= rb0 && rb < rb1) {
 #pragma unroll
       for (int gg = 0; gg < 4; ++gg) {
         double bc[2][4];
@@ -220,7 +224,7 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
   // subtracted from X once (LAPACK-like rounding of the large operand)
 #pragma unroll
   for (int rb = 0; rb < NB / IB; ++rb) {
-    if (rb >= rb0 && rb < rb1) {
+    if (rb >= RBL && rb < RBH && rb >= rb0 && rb < rb1) {
       double acc3[4][2];
 #pragma unroll
       for (int gg = 0; gg < 4; ++gg) acc3[gg][0] = acc3[gg][1] = 0.0;
@@ -259,7 +263,8 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
 }
 
 // x rows [8*g0, 8*g1) of the warp's columns (column-major tile, ld NB)
-template <int NB>
+// (ZERO: clear the other rows; else leave them untouched)
+template <int NB, bool ZERO = true>
 __device__ __forceinline__ void load_x(double (&x)[NB / 8][2], const double* col, int g0, int g1, int lane) {
   const int r = lane >> 2, c = lane & 3;
 #pragma unroll
@@ -268,7 +273,7 @@ __device__ __forceinline__ void load_x(double (&x)[NB / 8][2], const double* col
       double2 v = ldcg2(col + r * NB + 8 * g + 2 * c);
       x[g][0] = v.x;
       x[g][1] = v.y;
-    } else {
+    } else if (ZERO) {
       x[g][0] = x[g][1] = 0.0;
     }
   }

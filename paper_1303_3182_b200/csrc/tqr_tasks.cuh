@@ -98,10 +98,10 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
   const int warp = tid >> 5, lane = tid & 31;
   UPROF_DECL;
   const int col0 = slab * WS + warp * 8;
+  double* const xc = xt + size_t(col0) * NB;
   double x[NB / 8][2];
-  load_x<NB>(x, xt + size_t(col0) * NB, 0, NB / 8, lane);
-  UPROF_MARK(8);
-  for (int s = 0; s < NBLK; ++s) {
+  // one reflector block: wait for its staged V/T, apply, release the buffer
+  auto block = [&](int s, auto rbl, auto rbh) {
     const unsigned q = seq + unsigned(s), buf = q & 1u;
     const int b = TRANST ? s : NBLK - 1 - s;
     mbar_wait(&full[buf], (q >> 1) & 1u);
@@ -112,12 +112,41 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
     const double* Ts = sm + (buf ? S::U_T1 : S::U_T0);
     double* top = (MODE == GE) ? nullptr : topt + size_t(col0) * NB + b * IB;
     const double* top_s = (MODE == GE) ? nullptr : sm + (buf ? S::U_P1 : S::U_P0) + warp * 8 * IB;
-    warp_apply<NB, TRANST, MODE>(x, r0 / IB, r1 / IB, Vs, Ts, top, lane, top_s, b);
+    warp_apply<NB, TRANST, MODE, decltype(rbl)::value, decltype(rbh)::value>(x, r0 / IB, r1 / IB, Vs, Ts, top, lane,
+                                                                             top_s, b);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[buf]);
     UPROF_MARK(2);
+  };
+  using R0 = std::integral_constant<int, 0>;
+  using RH = std::integral_constant<int, NBLK / 2>;
+  using RN = std::integral_constant<int, NBLK>;
+  constexpr int GH = NB / 16;  // x row groups of the upper half
+  if constexpr (TRANST && MODE == TT) {
+    // Q^T with an upper-triangular V: block b only reads x rows of blocks
+    // <= b, so the lower half of X is still loading while blocks < NBLK/2 run
+    load_x<NB, false>(x, xc, 0, GH, lane);
+    load_x<NB, false>(x, xc, GH, NB / 8, lane);
+    UPROF_MARK(8);
+    for (int s = 0; s < NBLK / 2; ++s) block(s, R0{}, RH{});
+    for (int s = NBLK / 2; s < NBLK; ++s) block(s, R0{}, RN{});
+    store_x<NB>(x, xc, 0, NB / 8, lane);
+  } else if constexpr (TRANST && MODE == GE) {
+    // Q^T with a unit-lower V: rows of blocks < b are final once block b
+    // starts, so the upper half of X is stored while blocks >= NBLK/2 run
+    load_x<NB, false>(x, xc, 0, GH, lane);
+    load_x<NB, false>(x, xc, GH, NB / 8, lane);
+    UPROF_MARK(8);
+    for (int s = 0; s < NBLK / 2; ++s) block(s, R0{}, RN{});
+    store_x<NB>(x, xc, 0, GH, lane);
+    for (int s = NBLK / 2; s < NBLK; ++s) block(s, RH{}, RN{});
+    store_x<NB>(x, xc, GH, NB / 8, lane);
+  } else {
+    load_x<NB>(x, xc, 0, NB / 8, lane);
+    UPROF_MARK(8);
+    for (int s = 0; s < NBLK; ++s) block(s, R0{}, RN{});
+    store_x<NB>(x, xc, 0, NB / 8, lane);
   }
-  store_x<NB>(x, xt + size_t(col0) * NB, 0, NB / 8, lane);
   UPROF_MARK(6);
 }
 

@@ -132,10 +132,17 @@ struct NoPf {
 // GEMMs.
 // [RBL, RBH): compile-time bound on the row blocks this instance may touch,
 // so that x registers outside it can be in flight (loads) meanwhile.
-template <int NB, bool TRANST, int TRI = 2, int RBL = 0, int RBH = NB / IB, class PF = NoPf>
+// mid(x) runs once the first GEMM has consumed rows of blocks < NB/IB/2
+// (e.g. to issue the loads of the other half of X only then).
+struct NoMid {
+  template <class X>
+  __device__ __forceinline__ void operator()(X&) const {}
+};
+template <int NB, bool TRANST, int TRI = 2, int RBL = 0, int RBH = NB / IB, class PF = NoPf, class MID = NoMid>
 __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int rb1, const double* __restrict__ Vs,
                                            const double* __restrict__ Ts, double* top, int lane,
-                                           const double* top_s = nullptr, int drb = -1, PF pf = PF()) {
+                                           const double* top_s = nullptr, int drb = -1, PF pf = PF(),
+                                           MID mid = MID()) {
   // is V sub-block (row group gg, column group cb) of the diagonal block zero?
   auto zero_blk = [](int gg, int cb) { return TRI == 0 ? (gg < cb) : (TRI == 1 ? (gg > cb) : false); };
   const int r = lane >> 2, c = lane & 3;
@@ -181,6 +188,7 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
         pf();
       }
     }
+    if (rb == NB / IB / 2 - 1) mid(x);
   }
   if (top) {
 #pragma unroll

@@ -101,7 +101,7 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
   double* const xc = xt + size_t(col0) * NB;
   double x[NB / 8][2];
   // one reflector block: wait for its staged V/T, apply, release the buffer
-  auto block = [&](int s, auto rbl, auto rbh) {
+  auto block = [&](int s, auto rbl, auto rbh, auto mid) {
     const unsigned q = seq + unsigned(s), buf = q & 1u;
     const int b = TRANST ? s : NBLK - 1 - s;
     mbar_wait(&full[buf], (q >> 1) & 1u);
@@ -113,7 +113,7 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
     double* top = (MODE == GE) ? nullptr : topt + size_t(col0) * NB + b * IB;
     const double* top_s = (MODE == GE) ? nullptr : sm + (buf ? S::U_P1 : S::U_P0) + warp * 8 * IB;
     warp_apply<NB, TRANST, MODE, decltype(rbl)::value, decltype(rbh)::value>(x, r0 / IB, r1 / IB, Vs, Ts, top, lane,
-                                                                             top_s, b);
+                                                                             top_s, b, NoPf(), mid);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[buf]);
     UPROF_MARK(2);
@@ -122,29 +122,35 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
   using RH = std::integral_constant<int, NBLK / 2>;
   using RN = std::integral_constant<int, NBLK>;
   constexpr int GH = NB / 16;  // x row groups of the upper half
+  // loads of one half of X are issued only after the first use of the other
+  // half (all loads in flight share one scoreboard, so the first DMMA would
+  // otherwise wait for every one of them)
+  auto load_lower = [&](auto&) { load_x<NB, false>(x, xc, GH, NB / 8, lane); };
   if constexpr (TRANST && MODE == TT) {
     // Q^T with an upper-triangular V: block b only reads x rows of blocks
-    // <= b, so the lower half of X is still loading while blocks < NBLK/2 run
+    // <= b, so the lower half of X loads while the first blocks run
     load_x<NB, false>(x, xc, 0, GH, lane);
-    load_x<NB, false>(x, xc, GH, NB / 8, lane);
     UPROF_MARK(8);
-    for (int s = 0; s < NBLK / 2; ++s) block(s, R0{}, RH{});
-    for (int s = NBLK / 2; s < NBLK; ++s) block(s, R0{}, RN{});
+    block(0, R0{}, RH{}, NoMid());
+    load_lower(x);
+    for (int s = 1; s < NBLK / 2; ++s) block(s, R0{}, RH{}, NoMid());
+    for (int s = NBLK / 2; s < NBLK; ++s) block(s, R0{}, RN{}, NoMid());
     store_x<NB>(x, xc, 0, NB / 8, lane);
   } else if constexpr (TRANST && MODE == GE) {
-    // Q^T with a unit-lower V: rows of blocks < b are final once block b
-    // starts, so the upper half of X is stored while blocks >= NBLK/2 run
+    // Q^T with a unit-lower V: the lower half of X loads while block 0 works
+    // on the upper half; rows of blocks < b are final once block b starts,
+    // so the upper half is stored while blocks >= NBLK/2 run
     load_x<NB, false>(x, xc, 0, GH, lane);
-    load_x<NB, false>(x, xc, GH, NB / 8, lane);
     UPROF_MARK(8);
-    for (int s = 0; s < NBLK / 2; ++s) block(s, R0{}, RN{});
+    block(0, R0{}, RN{}, load_lower);
+    for (int s = 1; s < NBLK / 2; ++s) block(s, R0{}, RN{}, NoMid());
     store_x<NB>(x, xc, 0, GH, lane);
-    for (int s = NBLK / 2; s < NBLK; ++s) block(s, RH{}, RN{});
+    for (int s = NBLK / 2; s < NBLK; ++s) block(s, RH{}, RN{}, NoMid());
     store_x<NB>(x, xc, GH, NB / 8, lane);
   } else {
     load_x<NB>(x, xc, 0, NB / 8, lane);
     UPROF_MARK(8);
-    for (int s = 0; s < NBLK; ++s) block(s, R0{}, RN{});
+    for (int s = 0; s < NBLK; ++s) block(s, R0{}, RN{}, NoMid());
     store_x<NB>(x, xc, 0, NB / 8, lane);
   }
   UPROF_MARK(6);

@@ -49,6 +49,7 @@ __device__ unsigned long long g_uprof[16];
 
 constexpr int NT = 256;  // compute threads per CTA (8 warps)
 constexpr int NW = 8;
+constexpr int TLD = 40;  // ld of the staged pivot rows (IB + 8: conflict-free 16-byte reads)
 constexpr int NTP = NT + 128;  // + one producer warpgroup (staging / prefetch)
 
 // all threads of the CTA (both warp roles)
@@ -149,12 +150,12 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
   const int s1a = swz_in(2 * c, r), s1b = swz_in(2 * c + 1, r);  // (2c+h, r)
   const int s3a = swz_in(r, 2 * c), s3b = swz_in(r, 2 * c + 1);  // (r, 2c+h)
   // top_s: the block's IB pivot rows of this warp's 8 columns staged in smem
-  // (column-major, ld IB); else read from global
+  // (column-major, ld TLD); else read from global
   double w[4][2], ap[4][2];
   if (top) {
 #pragma unroll
     for (int nb = 0; nb < 4; ++nb) {
-      double2 v = top_s ? *reinterpret_cast<const double2*>(top_s + 8 * nb + 2 * c + r * IB)
+      double2 v = top_s ? *reinterpret_cast<const double2*>(top_s + 8 * nb + 2 * c + r * TLD)
                         : ldcg2(top + 8 * nb + 2 * c + r * NB);
       ap[nb][0] = v.x;
       ap[nb][1] = v.y;
@@ -355,13 +356,13 @@ __device__ __forceinline__ void pstage_t(double* Ts, const double* __restrict__ 
 }
 
 // IB pivot rows [r0, r0+IB) of WS columns from col0 (ld NB) -> smem,
-// column-major ld IB, 16-byte copies
+// column-major ld TLD, 16-byte copies
 template <int NB>
 __device__ __forceinline__ void pstage_top(double* dst, const double* __restrict__ tile, int col0, int r0, int pw,
                                            int lane) {
   for (int e = pw * 32 + lane; e < WS * (IB / 2); e += NPW * 32) {
     const int cc = e / (IB / 2), rr = (e % (IB / 2)) * 2;
-    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst + rr + cc * IB));
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst + rr + cc * TLD));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(tile + size_t(col0 + cc) * NB + r0 + rr));
   }
 }

@@ -221,6 +221,12 @@ void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers
     }
   std::vector<double> w(n), prio(n, 0.0);
   for (size_t v = 0; v < n; ++v) w[v] = item_cost(items[v].kind, nb);
+  // simulated durations: the panel cost may differ from the one the
+  // priorities use (TQR_SIM_PANEL: panel items' duration multiplier)
+  static const double sim_panel = env_cost("TQR_SIM_PANEL", 1.0);
+  std::vector<double> wd(w);
+  for (size_t v = 0; v < n; ++v)
+    if (items[v].kind <= tqr::TSQRT) wd[v] = w[v] * sim_panel;
   for (size_t v = n; v-- > 0;) {  // items are in a topological order already
     double best = 0.0;
     for (int32_t k = nsucc[v]; k < nsucc[v + 1]; ++k) best = std::max(best, prio[size_t(succ[size_t(k)])]);
@@ -263,7 +269,7 @@ void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers
       const int32_t v = ready.top().second;
       ready.pop();
       order.push_back(v);
-      running.emplace(now + w[size_t(v)], v);
+      running.emplace(now + wd[size_t(v)], v);
       --idle;
     }
     if (running.empty() && pending.empty()) break;  // cannot happen for a DAG

@@ -16,7 +16,7 @@ struct Smem {
   static constexpr int VS = NB * IB;  // one staged V block
   static constexpr int TS = IB * IB;
   // update layout
-  static constexpr int TOP = IB * WS;  // staged pivot rows of a slab (TT/TS)
+  static constexpr int TOP = TLD * WS;  // staged pivot rows of a slab (TT/TS)
   static constexpr int U_V0 = 0, U_V1 = VS, U_T0 = 2 * VS, U_T1 = 2 * VS + TS, U_P0 = 2 * VS + 2 * TS,
                        U_P1 = U_P0 + TOP, U_END = U_P1 + TOP;
   // panel layout: stacked panel P (column-major, ld PLD = 4 mod 16), staged
@@ -111,7 +111,7 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
     const double* Vs = sm + (buf ? S::U_V1 : S::U_V0);
     const double* Ts = sm + (buf ? S::U_T1 : S::U_T0);
     double* top = (MODE == GE) ? nullptr : topt + size_t(col0) * NB + b * IB;
-    const double* top_s = (MODE == GE) ? nullptr : sm + (buf ? S::U_P1 : S::U_P0) + warp * 8 * IB;
+    const double* top_s = (MODE == GE) ? nullptr : sm + (buf ? S::U_P1 : S::U_P0) + warp * 8 * TLD;
     warp_apply<NB, TRANST, MODE, decltype(rbl)::value, decltype(rbh)::value>(x, r0 / IB, r1 / IB, Vs, Ts, top, lane,
                                                                              top_s, b, NoPf(), mid);
     __syncwarp();

@@ -336,16 +336,24 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
         // every warp: lane v (mod 8) sums value v over the warps and computes
         // the reflector scalars redundantly (no second barrier)
         const int v = lane & 7;
-        double D = 0.0;
+        double pw[NW];
 #pragma unroll
-        for (int w = 0; w < NW; ++w) D += partj[w * 8 + v];
+        for (int w = 0; w < NW; ++w) pw[w] = partj[w * 8 + v];
+#pragma unroll
+        for (int h = NW / 2; h >= 1; h >>= 1)
+#pragma unroll
+          for (int w = 0; w < h; ++w) pw[w] += pw[w + h];
+        const double D = pw[0];
         const double alpha = drowj[jj];
         const double xn2 = __shfl_sync(0xffffffffu, D, jj);
         double tau = 0.0, scal = 0.0, beta = alpha;
         if (xn2 != 0.0) {
           beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-          tau = (beta - alpha) / beta;
-          scal = 1.0 / (alpha - beta);
+          // dlarfg's tau = (beta - alpha) / beta and 1 / (alpha - beta) from
+          // one division
+          const double am = alpha - beta, rr = 1.0 / (am * beta);
+          tau = -(am * am) * rr;
+          scal = beta * rr;
         }
         const double sv = tau * (drowj[v] + scal * D);
         if (tid == 0) {

@@ -156,6 +156,24 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
   UPROF_MARK(6);
 }
 
+#ifdef TQR_PROF_L2
+__device__ unsigned long long g_l2prof[8];
+#define L2P_DECL long long _l2t = clock64()
+#define L2P_MARK(k)                                                         \
+  do {                                                                      \
+    if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 224)) {     \
+      const long long _n = clock64();                                       \
+      atomicAdd(&g_l2prof[(k) + (threadIdx.x ? 4 : 0)], (unsigned long long)(_n - _l2t)); \
+      _l2t = _n;                                                            \
+    }                                                                       \
+  } while (0)
+#else
+#define L2P_DECL
+#define L2P_MARK(k) \
+  do {              \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------------------
 // panel item: Householder QR of one tile (GE), of [R_piv; R_i] (TT) or of
 // [R_piv; A_i] (TS), ib = 32 columns at a time, each block in four groups of
@@ -212,13 +230,25 @@ __device__ __noinline__ void panel_trailing(double* at, double* rt, const double
   const int nch = (NB - rb0 - IB) / 8;
   const int g0 = (MODE == GE) ? rb0 / 8 : 0;
   const int g1 = (MODE == TT) ? (rb0 + IB) / 8 : NB / 8;
+  constexpr int GH = NB / 16;  // row groups of the upper half
+  // the rows of the lower half load while the first GEMM runs on the upper
+  // half (own scoreboard: see update_consume) when the block spans both
+  const bool split = g0 < GH && g1 > GH;
   for (int ch = warp; ch < nch; ch += NW) {
     const int col = rb0 + IB + ch * 8;
+    double* const xc = at + size_t(col) * NB;
     double x[NB / 8][2];
-    load_x<NB>(x, at + size_t(col) * NB, g0, g1, lane);
     double* top = (MODE == GE) ? nullptr : rt + size_t(col) * NB + rb0;
-    warp_apply<NB, true, (MODE == TS ? 2 : MODE)>(x, g0 / (IB / 8), g1 / (IB / 8), Vs, Ts, top, lane, nullptr, b);
-    store_x<NB>(x, at + size_t(col) * NB, g0, g1, lane);
+    if (split) {
+      load_x<NB>(x, xc, g0, GH, lane);
+      auto lower = [&](auto&) { load_x<NB, false>(x, xc, GH, g1, lane); };
+      warp_apply<NB, true, (MODE == TS ? 2 : MODE), 0, NB / IB, NoPf, decltype(lower)>(
+          x, g0 / (IB / 8), g1 / (IB / 8), Vs, Ts, top, lane, nullptr, b, NoPf(), lower);
+    } else {
+      load_x<NB>(x, xc, g0, g1, lane);
+      warp_apply<NB, true, (MODE == TS ? 2 : MODE)>(x, g0 / (IB / 8), g1 / (IB / 8), Vs, Ts, top, lane, nullptr, b);
+    }
+    store_x<NB>(x, xc, g0, g1, lane);
   }
 }
 
@@ -296,6 +326,7 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
       }
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) {
+        L2P_DECL;
         const int j = c0 + jj;
         double* partj = part + (jj & 1) * (NW * 8);  // double-buffered by column parity
         double* drowj = drow + (jj & 1) * 8;
@@ -332,7 +363,9 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
           d[0] += __shfl_xor_sync(0xffffffffu, d[0], 1);
           if ((lane & 3) == 0) partj[warp * 8 + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = d[0];
         }
+        L2P_MARK(0);
         csync();
+        L2P_MARK(1);
         // every warp: lane v (mod 8) sums value v over the warps and computes
         // the reflector scalars redundantly (no second barrier)
         const int v = lane & 7;
@@ -355,6 +388,7 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
           tau = -(am * am) * rr;
           scal = beta * rr;
         }
+        L2P_MARK(2);
         const double sv = tau * (drowj[v] + scal * D);
         if (tid == 0) {
           tau_s[j] = tau;
@@ -383,6 +417,7 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
           }
         }
         if (t == j) rv0[jj] = beta;
+        L2P_MARK(3);
         mark(7);
       }
 #pragma unroll

@@ -63,6 +63,15 @@ void run(const char* name, int sms) {
   printf("{\"panel\": \"%s\", \"nb\": %d, \"us_per_panel\": %.1f, \"phases_us\": {", name, NB, per);
   for (int i = 0; i < 9; ++i) printf("%s\"%s\": %.1f", i ? ", " : "", nm[i], hp[MODE * 16 + i] / 1e3 / reps);
   printf("}, \"err\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
+#ifdef TQR_PROF_L2
+  unsigned long long l2[8];
+  cudaMemcpyFromSymbol(l2, g_l2prof, sizeof(l2));
+  const double cols = double(NB) * reps;
+  printf("  level-2 cycles/column warp0: products+reduce %.0f  barrier %.0f  scalars %.0f  update %.0f | warp7: %.0f %.0f %.0f %.0f\n",
+         l2[0] / cols, l2[1] / cols, l2[2] / cols, l2[3] / cols, l2[4] / cols, l2[5] / cols, l2[6] / cols, l2[7] / cols);
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(g_l2prof, z, sizeof(z));
+#endif
   cudaFree(tiles);
   cudaFree(ts);
   cudaFree(prof);

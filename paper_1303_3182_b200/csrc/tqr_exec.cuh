@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
             }
             if (ok) __threadfence();  // drop stale L1 lines before cp.async.ca reads
             s_early = ok;
+            if (P.trace) atomicAdd(P.trace + 4 * size_t(P.n_items) + 56 + (ok ? 0 : 1), 1ull);
           }
           asm volatile("bar.sync 2, 128;\n" ::: "memory");
           pre = s_early;
@@ -300,9 +301,11 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
         break;
     }
     if (is_update_kind(I.kind)) seq += NBLK;
-    __threadfence();
+    // publish: the CTA barrier orders every thread's stores before thread 0's
+    // gpu-scope fence, which (cumulatively) orders them before the flag
     bar_all();
     if (tid == 0) {
+      __threadfence();
       st_release(P.done + it, 1);
       if (P.trace) {
         P.trace[4 * size_t(it)] = t_deq;

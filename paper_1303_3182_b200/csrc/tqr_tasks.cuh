@@ -104,7 +104,9 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
   auto block = [&](int s, auto rbl, auto rbh, auto mid) {
     const unsigned q = seq + unsigned(s), buf = q & 1u;
     const int b = TRANST ? s : NBLK - 1 - s;
+#ifndef TQR_ABL_NOPROD
     mbar_wait(&full[buf], (q >> 1) & 1u);
+#endif
     UPROF_MARK(0);
     int r0, r1;
     upd_rows<NB, MODE>(b, r0, r1);
@@ -115,7 +117,9 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
     warp_apply<NB, TRANST, MODE, decltype(rbl)::value, decltype(rbh)::value>(x, r0 / IB, r1 / IB, Vs, Ts, top, lane,
                                                                              top_s, b, NoPf(), mid);
     __syncwarp();
+#ifndef TQR_ABL_NOPROD
     if (lane == 0) mbar_arrive(&empty[buf]);
+#endif
     UPROF_MARK(2);
   };
   using R0 = std::integral_constant<int, 0>;

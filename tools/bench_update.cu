@@ -34,8 +34,10 @@ __global__ void __launch_bounds__(NTP, 1) k_upd(double* tiles, double* tt, int r
         prefetch_l2(base + T2 + size_t(ns) * WS * NB, WS * NB * 8);
         prefetch_l2(base + 2 * T2 + size_t(ns) * WS * NB, WS * NB * 8);
       }
+#ifndef TQR_ABL_NOPROD
       update_produce<NB, MODE, true>(sm, base, tt, base + 2 * T2, r % (NB / WS), warp - NW, threadIdx.x & 31, bars,
                                      bars + 2, seq);
+#endif
       seq += NB / IB;
       bar_all();
     }

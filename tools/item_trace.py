@@ -114,6 +114,7 @@ def main():
         if cnt:
             out.setdefault("panel_phases_us", {})[nm] = {names[k]: round(float(prof[md * 16 + k]) / 1e3 / cnt, 2)
                                                         for k in range(len(names))}
+    out["early_staging"] = {"staged": int(prof[56]), "not_ready": int(prof[57])}
     nsm = int(sm.max()) + 1
     busy = (end - rdy).sum()
     waits = (rdy - deq).sum()

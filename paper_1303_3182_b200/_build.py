@@ -19,6 +19,8 @@ OUT = os.path.join(HERE, "libtqr.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXXFLAGS = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "-I", os.path.join(ROOT, "include")]
+# experiment hook (ablation macros); changing it requires a clean build/
+CXXFLAGS += os.environ.get("TQR_EXTRA_NVCC_FLAGS", "").split()
 HEADERS = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh"))] + \
     [os.path.join(ROOT, "include", "tqr.h")]
 

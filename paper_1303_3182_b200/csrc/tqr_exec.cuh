@@ -173,7 +173,10 @@ __device__ __forceinline__ bool is_update_kind(int k) { return k == tqr::UNMQR |
 // Warp-specialized persistent executor.  Warpgroups 0-1 (8 warps, 232
 // registers) run the kernels; warpgroup 2 (40 registers) stages reflector
 // blocks for update items (warp 8) and prefetches the next item's tiles into
-// L2 (warp 9).  Per item both roles pass the same three CTA barriers.
+// L2 (warp 9).  Per item the roles meet at one CTA barrier (item
+// finished); the consumers check dependencies on their own barrier and the
+// producer publishes completion flags, so neither waits for the other's
+// memory fences.
 template <int NB, bool TRANST>
 __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
   extern __shared__ __align__(16) double sm[];
@@ -210,14 +213,27 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
         update_produce<NB, TS, TRANST>(sm, vt, P.te + soff<NB>(P.p, J.i, J.k), P.tiles + toff<NB>(P.p, J.piv, J.j),
                                        J.slab, pw, lane, bars, bars + 2, sq, s_begin, s_end);
     };
+    int it = s_cur, nx = s_nxt;
     for (;;) {
-      const int it = s_cur, nx = s_nxt;
       if (it >= P.n_items) break;
       const Item I = P.items[it];
-      bar_all();  // dependencies satisfied
       if (warp == NW && lane == 0 && nx < P.n_items) prefetch_item<NB>(P, P.items[nx]);
       const bool upd = is_update_kind(I.kind);
-      if (upd) produce(I, pre ? 1 : 0, NBLK, seq);
+      if (upd) {
+        if (!pre) {
+          // not staged early: wait for the item's predecessors here (the
+          // consumers check them too, on their own barrier)
+          if (tid == NT) {
+            for (int t = 0; t < I.pred_n; ++t) {
+              const int pr = P.preds[I.pred_lo + t];
+              while (ld_acquire(P.done + pr) == 0) __nanosleep(40);
+            }
+            __threadfence();  // drop stale L1 lines before cp.async.ca reads
+          }
+          asm volatile("bar.sync 2, 128;\n" ::: "memory");
+        }
+        produce(I, pre ? 1 : 0, NBLK, seq);
+      }
       unsigned seq_next = seq + (upd ? NBLK : 0);
       // stage block 0 of the next update item now if its predecessors are
       // already done (non-blocking; never when it depends on this item)
@@ -242,14 +258,23 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
         }
       }
       seq = seq_next;
-      bar_all();  // item finished
-      bar_all();  // next item published
+      bar_all();  // item finished: every consumer store of `it` is issued
+      const int done_it = it;
+      it = s_cur;
+      nx = s_nxt;
+      // publish `it` off the consumers' path: the CTA barrier orders their
+      // stores before this thread's gpu-scope fence (cumulative), which
+      // waits for them to drain; then the release flag
+      if (tid == NT) {
+        __threadfence();
+        st_release(P.done + done_it, 1);
+      }
     }
     return;
   }
   setmaxnreg_inc<232>();
+  int it = s_cur, nx = s_nxt;
   for (;;) {
-    const int it = s_cur, nx = s_nxt;
     if (it >= P.n_items) break;
     const Item I = P.items[it];
     unsigned long long t_deq = 0;
@@ -262,7 +287,7 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
       __syncwarp();
       __threadfence();  // gpu-scope fence: also drops stale L1 lines
     }
-    bar_all();
+    csync();  // dependencies satisfied (the producer checks them itself)
     unsigned long long t_rdy = 0;
     if (P.trace && tid == 0) t_rdy = gtimer();
     unsigned long long* pprof = P.trace ? P.trace + 4 * size_t(P.n_items) : nullptr;
@@ -301,12 +326,10 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
         break;
     }
     if (is_update_kind(I.kind)) seq += NBLK;
-    // publish: the CTA barrier orders every thread's stores before thread 0's
-    // gpu-scope fence, which (cumulatively) orders them before the flag
-    bar_all();
+    // take the item after next now; the producer warpgroup publishes `it`
+    // after the barrier (its fence waits for this CTA's stores to drain while
+    // the consumers already start the next item)
     if (tid == 0) {
-      __threadfence();
-      st_release(P.done + it, 1);
       if (P.trace) {
         P.trace[4 * size_t(it)] = t_deq;
         P.trace[4 * size_t(it) + 1] = t_rdy;
@@ -317,6 +340,8 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
       s_nxt = nx < P.n_items ? atomicAdd(P.queue, 1) : P.n_items;
     }
     bar_all();
+    it = s_cur;
+    nx = s_nxt;
   }
 }
 

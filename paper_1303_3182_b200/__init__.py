@@ -26,7 +26,7 @@ from .qr import (  # noqa: F401
 
 def __getattr__(name):
     # the numeric engine imports torch lazily so schedule users do not pay for it
-    if name in ("tiled_qr", "TiledQR", "Plan"):
+    if name in ("tiled_qr", "tiled_qr_host", "TiledQR", "Plan"):
         from . import engine
         return getattr(engine, name)
     raise AttributeError(name)

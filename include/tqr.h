@@ -124,9 +124,10 @@ int tqr_extract_r(const double* tiles, int p, int q, int nb, double* R, int64_t 
  * te_stride doubles per tile).  Asynchronous on `stream`.                  */
 int tqr_factor(tqr_plan* plan, double* tiles, double* tg, double* te, void* stream);
 /* Streaming factorization: a_src = row-major m x n input staging buffer in
- * device memory, filled asynchronously by the caller one nb-column block at
- * a time, each block followed by setting arrive[j] != 0 on the same copy
- * stream (e.g. cuStreamWriteValue32); arrive[] must be zero at launch.
+ * device memory, filled asynchronously by the caller one arrival unit at a
+ * time (tqr_plan_arrival_units: a block of tile rows of one tile column),
+ * each unit u followed by setting arrive[u] != 0 on the same copy stream
+ * (e.g. cuStreamWriteValue32); arrive[] (n_units ints) must be zero at launch.
  * r_dst = row-major n x n R (device-accessible), strictly-lower part outside
  * the diagonal tiles left untouched.  r_ready (optional, q ints, zero at
  * launch): r_ready[i] counts the tiles of R's tile row i+1 already written,
@@ -135,7 +136,8 @@ int tqr_factor_io(tqr_plan* plan, const double* a_src, int64_t lda, const int* a
                   double* te, double* r_dst, int64_t ldr, int* r_ready, void* stream);
 /* Host-to-host QR (plan made with io = 3): pinned row-major A (lda_h) in,
  * pinned row-major R (ldr_h) out, every transfer overlapped with the
- * factorization.  Enqueues on `stream` the executor, on `copy_in` the
+ * factorization.  With io = 1 only A streams in (r_host, r_dev, r_ready may
+ * be NULL; the factored tiles stay in `tiles`).  Enqueues on `stream` the executor, on `copy_in` the
  * nb-column blocks of A (one 2D copy each, in tqr_plan_arrival_order) each
  * followed by its arrival flag, and on `copy_out` one wait + copy per tile
  * row of R; returns at once, `stream` completes after all three.  Device
@@ -145,8 +147,11 @@ int tqr_factor_io(tqr_plan* plan, const double* a_src, int64_t lda, const int* a
 int tqr_qr_host(tqr_plan* plan, const double* a_host, int64_t lda_h, double* r_host, int64_t ldr_h, double* stage,
                 int* arrive, double* tiles, double* tg, double* te, double* r_dev, int* r_ready, void* stream,
                 void* copy_in, void* copy_out);
-/* 1-based tile columns in the order tqr_qr_host transfers them (q ints). */
-int tqr_plan_arrival_order(const tqr_plan* plan, int32_t* cols_out);
+/* Input arrival units of an io plan in transfer order: *n_units, and if
+ * units3 != NULL, 3 ints per unit: 1-based tile column j, first tile row i0,
+ * number of tile rows.  A unit's flag is arrive[(j-1)*nch + (i0-1)/cr] with
+ * cr the chunk height (units3[2] of the first unit) and nch = ceil(p/cr).   */
+int tqr_plan_arrival_units(const tqr_plan* plan, int32_t* n_units, int32_t* units3);
 /* C <- Q C (trans=0) or Q^T C (trans=1) for C stored as p x c_cols tiles,
  * replaying the trace's reflectors (forward for Q^T, reverse for Q).      */
 int tqr_apply_q(tqr_plan* plan, int trans, const double* tiles, const double* tg, const double* te,

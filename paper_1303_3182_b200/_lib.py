@@ -71,7 +71,7 @@ SIGNATURES = {
     "tqr_factor": (C.c_int, [vp, vp, vp, vp, vp]),
     "tqr_factor_io": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, C.c_int64, vp, vp]),
     "tqr_qr_host": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
-    "tqr_plan_arrival_order": (C.c_int, [vp, i32p]),
+    "tqr_plan_arrival_units": (C.c_int, [vp, i32p, i32p]),
     "tqr_apply_q": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, C.c_int, vp]),
     "tqr_fp64_peak": (C.c_int, [f64p, vp]),
     "tqr_set_trace": (C.c_int, [vp]),

@@ -205,7 +205,7 @@ inline double item_cost(int kind, int nb) {
 // reference's list scheduler (sched.py:77-156).  The result is a
 // topological order, which the executor's deadlock-freedom needs.
 void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers, int nb,
-              const std::vector<double>& col_release = {}) {
+              const std::vector<double>& unit_release = {}, int acr = 1, int anch = 1) {
   const size_t n = items.size();
   if (n == 0) return;
   std::vector<int32_t> nsucc(n + 1, 0);
@@ -238,9 +238,10 @@ void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers
     if (items[v].kind == tqr::UNPACK) prio[v] = 1e12;
   std::vector<int32_t> indeg(n);
   for (size_t v = 0; v < n; ++v) indeg[v] = items[v].pred_n;
-  // PACK(i,j) cannot start before tile column j has arrived (col_release[j-1])
+  // PACK(i,j) cannot start before its arrival unit has landed
   auto release = [&](size_t v) {
-    return items[v].kind == tqr::PACK && !col_release.empty() ? col_release[size_t(items[v].j - 1)] : 0.0;
+    if (items[v].kind != tqr::PACK || unit_release.empty()) return 0.0;
+    return unit_release[size_t((items[v].j - 1) * anch + (items[v].i - 1) / acr)];
   };
   using RQ = std::pair<double, int32_t>;  // (-priority, id) min-heap == max priority, lowest id
   std::priority_queue<RQ, std::vector<RQ>, std::greater<RQ>> ready;
@@ -324,7 +325,11 @@ struct tqr_plan {
   int64_t n_tasks = 0;
   double flops = 0;
   std::vector<Task> trace;  // factorization trace (for apply-Q)
-  std::vector<int32_t> arrival;  // io & 1: tile columns (1-based) in host transfer order
+  // io & 1: input arrival units in host transfer order, (column j, first
+  // tile row i0, tile rows) — tile column j split into row chunks of acr rows;
+  // unit (j, c) raises arrive[(j-1)*anch + c]
+  std::vector<int32_t> arrival;
+  int acr = 1, anch = 1;
   DevSched fac;
   std::map<std::pair<int, int>, DevSched> aq;  // (trans, c_cols) -> apply-Q schedule
   ~tqr_plan() {
@@ -459,14 +464,32 @@ int tqr_plan_create_io(const tqr_build* hb, int nb, int ib, int io, tqr_plan** o
       // host transfer order: tile columns left to right (the order the
       // factorization consumes them; a column block is one 2D copy at full
       // link rate), PACK(i,j) released when column j has landed
-      std::vector<double> col_release;
+      std::vector<double> unit_release;
       if (io & 1) {
-        for (int j = 1; j <= b.q; ++j) P->arrival.push_back(j);
-        // modeled arrival in item-cost units: one nb-column block of the m
-        // rows at ~50 GB/s host link; an update slab item ~ 54 us at nb=256
+        // tile columns left to right (the order the factorization consumes
+        // them), each in row chunks: up to 8, up to 64 when tall (p >= 4q).
+        // (Row-chunk-major order was measured worse at C5: the elimination
+        // tree pairs the top and bottom halves first.)
+        const bool tall = b.p >= 4 * b.q;
+        P->anch = std::min(b.p, tall ? 64 : 8);
+        P->acr = (b.p + P->anch - 1) / P->anch;
+        P->anch = (b.p + P->acr - 1) / P->acr;
+        auto unit = [&](int j, int c) {
+          const int i0 = 1 + c * P->acr;
+          P->arrival.insert(P->arrival.end(), {j, i0, std::min(P->acr, b.p - i0 + 1)});
+        };
+        for (int j = 1; j <= b.q; ++j)
+          for (int c = 0; c < P->anch; ++c) unit(j, c);
+        // modeled arrival (item-cost units, ~50 GB/s host link; an update
+        // slab item ~ 54 us at nb=256), indexed by flag (j-1)*anch + c
         const double unit_s = 54e-6 * (double(nb) / 256.0) * (double(nb) / 256.0);
-        const double col_s = double(nb) * double(b.p) * nb * 8.0 / 50e9;
-        for (int j = 1; j <= b.q; ++j) col_release.push_back(double(j) * col_s / unit_s);
+        unit_release.assign(size_t(b.q) * P->anch, 0.0);
+        double t = 0.0;
+        for (size_t u = 0; u < P->arrival.size() / 3; ++u) {
+          const int j = P->arrival[3 * u], c = (P->arrival[3 * u + 1] - 1) / P->acr;
+          t += double(P->arrival[3 * u + 2]) * nb * nb * 8.0 / 50e9 / unit_s;
+          unit_release[size_t(j - 1) * P->anch + c] = t;
+        }
       }
       const size_t m = tasks.size();
       // hazard edges of the reference model, weighted ASAP order (QR weights)
@@ -483,7 +506,7 @@ int tqr_plan_create_io(const tqr_build* hb, int nb, int ib, int io, tqr_plan** o
       std::vector<Item> items;
       std::vector<int32_t> preds;
       expand(tasks, in, order, nb / WS, items, preds);
-      cp_order(items, preds, num_sms_host(), nb, col_release);
+      cp_order(items, preds, num_sms_host(), nb, unit_release, P->acr, P->anch);
       upload(P->fac, items, preds);
       const double mm = double(b.p) * nb, nn = double(b.q) * nb;
       P->flops = 2.0 * nn * nn * (mm - nn / 3.0);
@@ -532,15 +555,16 @@ int tqr_factor_io(tqr_plan* P, const double* a_src, int64_t lda, const int* arri
     if ((P->io & 2) && !r_dst) throw tqr::ValueError("plan streams R out: r_dst needed");
   });
   if (rc) return rc;
-  IoBufs io{a_src, lda, arrive, r_dst, ldr, r_ready};
+  IoBufs io{a_src, lda, arrive, r_dst, ldr, r_ready, P->acr, P->anch};
   return cuda_guarded(run(P->fac, P->nb, true, tiles, tiles, tg, te, P->p, static_cast<cudaStream_t>(stream), io));
 }
 
-int tqr_plan_arrival_order(const tqr_plan* P, int32_t* cols_out) {
+int tqr_plan_arrival_units(const tqr_plan* P, int32_t* n_units, int32_t* units3) {
   return tqr::guard([&] {
     if (!P) throw tqr::ValueError("null plan");
     if (!(P->io & 1)) throw tqr::ValueError("plan does not stream its input");
-    std::copy(P->arrival.begin(), P->arrival.end(), cols_out);
+    if (n_units) *n_units = int32_t(P->arrival.size() / 3);
+    if (units3) std::copy(P->arrival.begin(), P->arrival.end(), units3);
   });
 }
 
@@ -549,9 +573,9 @@ int tqr_qr_host(tqr_plan* P, const double* a_host, int64_t lda_h, double* r_host
                 void* copy_in, void* copy_out) {
   int rc = tqr::guard([&] {
     if (!P) throw tqr::ValueError("null plan");
-    if (P->io != 3) throw tqr::ValueError("tqr_qr_host needs a plan made with io = 3");
-    if (!a_host || !r_host || !stage || !arrive || !r_dev || !r_ready)
-      throw tqr::ValueError("null buffer");
+    if (!(P->io & 1)) throw tqr::ValueError("tqr_qr_host needs a plan made with io & 1 (streamed input)");
+    if (!a_host || !stage || !arrive) throw tqr::ValueError("null buffer");
+    if ((P->io & 2) && (!r_host || !r_dev || !r_ready)) throw tqr::ValueError("null R buffer");
     if (!stream_memops()) throw std::runtime_error("CUDA stream memory operations unavailable");
   });
   if (rc) return rc;
@@ -577,27 +601,28 @@ int tqr_qr_host(tqr_plan* P, const double* a_host, int64_t lda_h, double* r_host
     cudaEventRecord(d0, st);
   }
   do {
-    if (ck(cudaMemsetAsync(arrive, 0, size_t(q) * sizeof(int), st))) break;
-    if (ck(cudaMemsetAsync(r_ready, 0, size_t(q) * sizeof(int), st))) break;
+    if (ck(cudaMemsetAsync(arrive, 0, P->arrival.size() / 3 * sizeof(int), st))) break;
+    if ((P->io & 2) && ck(cudaMemsetAsync(r_ready, 0, size_t(q) * sizeof(int), st))) break;
     if (ck(cudaEventRecord(ev0, st))) break;
     if (ck(cudaStreamWaitEvent(ci, ev0, 0)) || ck(cudaStreamWaitEvent(co, ev0, 0))) break;
-    IoBufs io{stage, n, arrive, r_dev, n, r_ready};
+    IoBufs io{stage, n, arrive, (P->io & 2) ? r_dev : nullptr, n, (P->io & 2) ? r_ready : nullptr, P->acr, P->anch};
     if (ck(run(P->fac, nb, true, tiles, tiles, tg, te, P->p, st, io))) break;
     if (dbg) cudaEventRecord(dk, st);
     bool bad = false;
-    // input: one nb-column block (m rows) per arrival, then raise its flag
-    // (the write value is ordered after the copy on the copy stream)
-    const size_t m = size_t(P->p) * nb;
-    for (int c : P->arrival) {
-      const size_t off = size_t(c - 1) * nb;
-      if ((bad = ck(cudaMemcpy2DAsync(stage + off, size_t(n) * 8, a_host + off, size_t(lda_h) * 8, size_t(nb) * 8, m,
-                                      cudaMemcpyHostToDevice, ci))))
+    // input: one (row chunk x nb columns) block per arrival unit, then raise
+    // its flag (the write value is ordered after the copy on the copy stream)
+    for (size_t u = 0; u < P->arrival.size() / 3; ++u) {
+      const size_t c0 = size_t(P->arrival[3 * u] - 1) * nb, r0 = size_t(P->arrival[3 * u + 1] - 1) * nb;
+      const size_t rows = size_t(P->arrival[3 * u + 2]) * nb;
+      if ((bad = ck(cudaMemcpy2DAsync(stage + r0 * size_t(n) + c0, size_t(n) * 8, a_host + r0 * size_t(lda_h) + c0,
+                                      size_t(lda_h) * 8, size_t(nb) * 8, rows, cudaMemcpyHostToDevice, ci))))
         break;
-      if ((bad = cu(g_write32(ci, arrive + (c - 1), 1)))) break;
+      const int fl = (P->arrival[3 * u] - 1) * P->anch + (P->arrival[3 * u + 1] - 1) / P->acr;
+      if ((bad = cu(g_write32(ci, arrive + fl, 1)))) break;
     }
     if (bad) break;
     // output: tile row i of R once its q-i+1 tiles are written out
-    for (int i = 1; i <= q && !bad; ++i) {
+    for (int i = 1; i <= q && !bad && (P->io & 2); ++i) {
       if ((bad = cu(g_wait32(co, r_ready + (i - 1), unsigned(q - i + 1))))) break;
       const size_t r0 = size_t(i - 1) * nb;
       bad = ck(cudaMemcpy2DAsync(r_host + r0 * size_t(ldr_h) + r0, size_t(ldr_h) * 8, r_dev + r0 * size_t(n) + r0,

@@ -35,10 +35,11 @@ struct ExecParams {
   // streaming I/O (PACK / UNPACK items)
   const double* a_src;  // row-major input staging (device), ld lda
   long long lda;
-  const int* arrive;  // per tile column: nonzero once its columns landed in a_src
+  const int* arrive;  // per arrival unit (tile column j, row chunk): nonzero once it landed in a_src
   double* r_dst;      // row-major R output (device-accessible), ld ldr
   long long ldr;
   int* r_ready;  // optional: per tile row of R, count of tiles written out
+  int acr, anch;  // arrival units: acr tile rows per chunk, anch chunks per tile column
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -92,8 +93,8 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
   return v;
 }
 
-// PACK(i,j): wait until tile column j of the row-major input has landed (the
-// host's copy stream raises arrive[j-1] after the column block), then transpose
+// PACK(i,j): wait until the arrival unit holding tile (i,j) of the row-major
+// input has landed (the host's copy stream raises its flag after the copy), then transpose
 // tile (i,j) into the tile-major, column-major-tile layout.  32-row chunks
 // through padded smem (LD = NB+1: both phases bank-conflict free); the next
 // chunk's loads are issued before the current chunk is written out.
@@ -101,7 +102,7 @@ template <int NB>
 __device__ void pack_item(double* sm, const ExecParams& P, int i, int j, int tid) {
   constexpr int CR = 32, LD = NB + 1, PER = CR * NB / NT;
   if (tid == 0) {
-    while (ld_acquire_sys(P.arrive + (j - 1)) == 0) __nanosleep(256);
+    while (ld_acquire_sys(P.arrive + (j - 1) * P.anch + (i - 1) / P.acr) == 0) __nanosleep(256);
   }
   csync();
   double* dst = P.tiles + toff<NB>(P.p, i, j);
@@ -354,6 +355,7 @@ struct IoBufs {
   double* r_dst = nullptr;
   long long ldr = 0;
   int* r_ready = nullptr;
+  int acr = 1, anch = 1;
 };
 
 struct DevView {
@@ -388,7 +390,7 @@ TQR_DECLARE_LAUNCH(256, false)
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));            \
     if (e != cudaSuccess) return e;                                                                                \
     ExecParams P{d.items,  d.preds, d.n_items, d.done,  d.queue,  vtiles,   tiles, tg,                              \
-                 te,       p,       trace,     g_flags, io.a_src, io.lda, io.arrive, io.r_dst, io.ldr, io.r_ready};           \
+                 te,       p,       trace,     g_flags, io.a_src, io.lda, io.arrive, io.r_dst, io.ldr, io.r_ready, io.acr, io.anch};           \
     kern<<<grid, NTP, smem, st>>>(P);                                                                               \
     return cudaGetLastError();                                                                                     \
   }

@@ -157,6 +157,28 @@ class GpuBackend:
         self.rbuf.view(self.q, self.q * t2).copy_(src)
         return self.rbuf
 
+    def factor_local_host(self, A_host):
+        """factor_local from a page-locked host shard: the column blocks
+        stream in on a copy stream while the executor factors (PACK items,
+        tqr_qr_host with io=1)."""
+        torch = self.torch
+        if getattr(self, "io_plan", None) is None:
+            from .engine import Plan
+            self.io_plan = Plan(self.local_plan.build, self.nb, io=Plan.IO_IN)
+            self.stage = torch.empty((self.P * self.nb, self.q * self.nb), dtype=torch.float64, device=self.dev)
+            self.arrive = torch.zeros(len(self.io_plan.arrival_units()), dtype=torch.int32, device=self.dev)
+            self.copy_in = torch.cuda.Stream(self.dev)
+        cs = torch.cuda.current_stream()
+        vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+        _lib.check(_lib.lib().tqr_qr_host(self.io_plan._h, C.c_void_p(A_host.data_ptr()), A_host.stride(0), None, 0,
+                                          vp(self.stage), vp(self.arrive), vp(self.tiles), vp(self.tg), vp(self.te),
+                                          None, None, C.c_void_p(cs.cuda_stream),
+                                          C.c_void_p(self.copy_in.cuda_stream), C.c_void_p(self.copy_in.cuda_stream)))
+        t2 = self.nb * self.nb
+        src = self.tiles.view(self.q, self.P * t2)[:, :self.q * t2]
+        self.rbuf.view(self.q, self.q * t2).copy_(src)
+        return self.rbuf
+
     def merge(self, r_a, r_b):
         """[R_a; R_b] -> merged R (q x q tiles, written into r_a)."""
         t2 = self.nb * self.nb
@@ -179,8 +201,13 @@ class GpuBackend:
 def tall_skinny_qr(A_local, backend, rank, world, dist=None):
     """Factor the block rows A_local on every rank; rank 0 returns the final
     q x q-tile R block (others return None).  `dist` is torch.distributed
-    (send/recv of the R block; NCCL on GPUs, gloo in the CPU tests)."""
-    r = backend.factor_local(A_local)
+    (send/recv of the R block; NCCL on GPUs, gloo in the CPU tests).
+    A_local on the host (page-locked, GpuBackend) streams in while the local
+    factorization runs."""
+    if getattr(A_local, "is_cuda", True) or not hasattr(backend, "factor_local_host"):
+        r = backend.factor_local(A_local)
+    else:
+        r = backend.factor_local_host(A_local)
     recv = None
     for stride, pairs in merge_rounds(world):
         for a, b in pairs:
@@ -243,6 +270,49 @@ def bench_main(args, cfg, make_matrix, Clocks, cpu_replay_rate):
         td.all_reduce(t, op=td.ReduceOp.MAX)
     ms = float(t.item())
     clocks = clk.stop() if clk else None
+    # e2e through the public API: each rank's shard H2D from (registered,
+    # page-locked) host memory, the factorization, R back to the host
+    e2e = None
+    if not getattr(args, "no_e2e", False):
+        import ctypes as C
+        cudart = torch.cuda.cudart()
+        host = torch.from_numpy(A_host)
+        reg = int(cudart.cudaHostRegister(host.data_ptr(), host.numel() * 8, 0)) == 0
+        R_host = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        ne = max(1, min(args.steps, 2))
+
+        def e2e_step():
+            out = tall_skinny_qr(host if reg else host.to(dev), be, rank, world, td if world > 1 else None)
+            if rank == 0:
+                R_host.copy_(be.r_matrix(out), non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            td.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(ne):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1) / ne], dtype=torch.float64, device=dev)
+        if world > 1:
+            td.all_reduce(te, op=td.ReduceOp.MAX)
+        if reg:
+            cudart.cudaHostUnregister(host.data_ptr())
+        e_ms = float(te.item())
+        e2e = {"value": round(flops / (e_ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s", "ms_per_step": round(e_ms, 3),
+               "api": "dist.tall_skinny_qr (page-locked host shard streamed in, R to host on rank 0)",
+               "h2d_bytes_per_step": int(m) * int(n) * 8, "d2h_bytes_per_step": int(n) * int(n) * 8,
+               "host_registered": reg}
+    peak = None
+    if rank == 0:
+        import ctypes as C
+        from . import _lib
+        pk = C.c_double()
+        _lib.check(_lib.lib().tqr_fp64_peak(C.byref(pk), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        peak = pk.value * world
     if rank == 0:
         R = be.r_matrix(out)
         ok = bool(torch.isfinite(R).all().item())
@@ -261,7 +331,11 @@ def bench_main(args, cfg, make_matrix, Clocks, cpu_replay_rate):
                        "parallelism": f"block rows over {world} GPU(s), NCCL p2p R merges",
                        "l2": "inputs > 126 MB L2 (no flush needed)"},
             "gpu_launches": (2 + 3 * (world - 1)) * args.steps,
-            "clocks": clocks, "cpu_baseline": cpu, "e2e": None,
+            "roofline": {"bound": "tensor", "achieved": round(flops / (ms * 1e-3) / 1e12, 3), "peak": round(peak, 3),
+                         "unit": "TFLOP/s", "frac": round(flops / (ms * 1e-3) / 1e12 / peak, 4), "traffic": None,
+                         "kernel": "exec_kernel (local factorization + merges)",
+                         "peak_source": "live DMMA.8x8x4 probe x n_gpus"},
+            "clocks": clocks, "cpu_baseline": cpu, "e2e": e2e,
             "check": {"r_finite": ok},
         }))
     if world > 1:

@@ -82,8 +82,9 @@ class Plan:
 
     def factor_stream(self, A_host, R_host, bufs):
         """Host-to-host factorization with every transfer overlapped
-        (tqr_qr_host): the nb-column blocks of the pinned row-major A_host
-        go up in arrival_order() on one copy stream, PACK items consume them as
+        (tqr_qr_host): the arrival units (row chunks of tile columns) of the
+        pinned row-major A_host go up in arrival_units() order on one copy
+        stream, PACK items consume them as
         they land, UNPACK items write finished R tiles to a device R and a
         second copy stream ships each tile row of R into the pinned R_host
         as soon as it is complete (zeros strictly below the diagonal tiles
@@ -103,19 +104,20 @@ class Plan:
         dev = device or torch.device("cuda", torch.cuda.current_device())
         tiles, tg, te = self.alloc(dev)
         return StreamBuffers(tiles, tg, te, torch.empty((self.m, self.n), dtype=torch.float64, device=dev),
-                             torch.zeros(self.q, dtype=torch.int32, device=dev),
+                             torch.zeros(len(self.arrival_units()), dtype=torch.int32, device=dev),
                              torch.empty((self.n, self.n), dtype=torch.float64, device=dev),
                              torch.zeros(self.q, dtype=torch.int32, device=dev),
                              torch.cuda.Stream(dev), torch.cuda.Stream(dev))
 
-    def arrival_order(self):
-        """1-based tile columns in host transfer order
-        (tqr_plan_arrival_order): left to right, as the factorization
-        consumes them."""
+    def arrival_units(self):
+        """Input arrival units in host transfer order (tqr_plan_arrival_units):
+        (tile column j, first tile row i0, tile rows), 1-based."""
         import numpy as np
-        out = np.empty(self.q, dtype=np.int32)
-        check(lib().tqr_plan_arrival_order(self._h, _lib.ptr_i32(out)))
-        return out.tolist()
+        n = C.c_int32()
+        check(lib().tqr_plan_arrival_units(self._h, C.byref(n), None))
+        out = np.empty(3 * n.value, dtype=np.int32)
+        check(lib().tqr_plan_arrival_units(self._h, C.byref(n), _lib.ptr_i32(out)))
+        return [tuple(int(v) for v in out[3 * u:3 * u + 3]) for u in range(n.value)]
 
     def apply_q(self, trans, tiles, tg, te, c_tiles, c_cols, stream=None):
         check(lib().tqr_apply_q(self._h, int(bool(trans)), _vp(tiles), _vp(tg), _vp(te), _vp(c_tiles),

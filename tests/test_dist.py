@@ -136,3 +136,18 @@ def test_gpu_emulated_shards(G, p, q, nb):
     R = row_sign_normalize(be.r_matrix(r).cpu().numpy())
     Rref = row_sign_normalize(np.linalg.qr(A, mode="r"))
     assert np.linalg.norm(R - Rref) <= 1e-11 * np.linalg.norm(A)
+
+
+@pytest.mark.gpu
+def test_gpu_streamed_local_factorization_matches_device_path():
+    """GpuBackend.factor_local_host (page-locked host shard streamed in with
+    PACK items) gives the same R block as factor_local on a device copy."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    P, q, nb = 16, 4, 64
+    A = _matrix(P, q, nb, seed=11)
+    be = dist.GpuBackend(P, q, nb, torch.device("cuda"))
+    r_dev = be.factor_local(torch.from_numpy(A).cuda()).clone()
+    r_host = be.factor_local_host(torch.from_numpy(A).pin_memory()).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(r_dev, r_host)

@@ -197,7 +197,8 @@ def test_c3_shape_residual_orthogonality(n):
     assert orth <= max(1e-12, 1.5 * REPLAY_ORTH[n]), orth
 
 
-@pytest.mark.parametrize("p,q,nb,algo", [(8, 4, 64, "greedy"), (6, 6, 256, "greedy"), (8, 2, 256, "fibonacci")])
+@pytest.mark.parametrize("p,q,nb,algo", [(8, 4, 64, "greedy"), (6, 6, 256, "greedy"), (8, 2, 256, "fibonacci"),
+                                         (20, 3, 64, "greedy"), (9, 9, 64, "flattree"), (70, 2, 64, "greedy")])
 def test_streaming_io_matches_device_path(p, q, nb, algo):
     """PACK/UNPACK work items (transfers overlapped with the factorization)
     give bit-identical R to the device-resident path."""
@@ -210,9 +211,18 @@ def test_streaming_io_matches_device_path(p, q, nb, algo):
 
 
 @pytest.mark.gpu
-def test_arrival_order_is_left_to_right_columns():
-    """tqr_qr_host ships tile columns left to right (the order the
-    factorization consumes them)."""
+def test_arrival_units_cover_tiles_column_major():
+    """tqr_qr_host ships tile columns left to right, each in row chunks,
+    covering every tile exactly once."""
     _need_gpu()
-    plan = Plan(P.build_tree(8, 4, "greedy"), 64, io=Plan.IO_IN | Plan.IO_OUT)
-    assert plan.arrival_order() == [1, 2, 3, 4]
+    for p, q in ((8, 4), (20, 3), (3, 3), (100, 4)):
+        plan = Plan(P.build_tree(p, q, "greedy"), 64, io=Plan.IO_IN | Plan.IO_OUT)
+        units = plan.arrival_units()
+        assert units == sorted(units)
+        seen = set()
+        for j, i0, nr in units:
+            for i in range(i0, i0 + nr):
+                assert (i, j) not in seen
+                seen.add((i, j))
+        assert seen == {(i, j) for i in range(1, p + 1) for j in range(1, q + 1)}
+        assert len(units) == q * len({(i0, nr) for _, i0, nr in units})

@@ -139,11 +139,12 @@ struct NoMid {
   template <class X>
   __device__ __forceinline__ void operator()(X&) const {}
 };
-template <int NB, bool TRANST, int TRI = 2, int RBL = 0, int RBH = NB / IB, class PF = NoPf, class MID = NoMid>
-__device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int rb1, const double* __restrict__ Vs,
-                                           const double* __restrict__ Ts, double* top, int lane,
-                                           const double* top_s = nullptr, int drb = -1, PF pf = PF(),
-                                           MID mid = MID()) {
+// One application of reflectors [8*KA, 8*KB) of the block (the 8-column
+// groups KA..KB-1): KA=0, KB=4 is the whole ib-block.
+template <int NB, bool TRANST, int TRI, int RBL, int RBH, int KA, int KB, class PF, class MID>
+__device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, int rb1, const double* __restrict__ Vs,
+                                             const double* __restrict__ Ts, double* top, int lane,
+                                             const double* top_s, int drb, PF& pf, MID& mid) {
   // is V sub-block (row group gg, column group cb) of the diagonal block zero?
   auto zero_blk = [](int gg, int cb) { return TRI == 0 ? (gg < cb) : (TRI == 1 ? (gg > cb) : false); };
   const int r = lane >> 2, c = lane & 3;
@@ -154,7 +155,7 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
   double w[4][2], ap[4][2];
   if (top) {
 #pragma unroll
-    for (int nb = 0; nb < 4; ++nb) {
+    for (int nb = KA; nb < KB; ++nb) {
       double2 v = top_s ? *reinterpret_cast<const double2*>(top_s + 8 * nb + 2 * c + r * TLD)
                         : ldcg2(top + 8 * nb + 2 * c + r * NB);
       ap[nb][0] = v.x;
@@ -165,7 +166,7 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
   // accumulate V^T X from zero and add the pivot rows once afterwards, as
   // LAPACK's dlarfb does (one rounding of the large operand per block)
 #pragma unroll
-  for (int nb = 0; nb < 4; ++nb) w[nb][0] = w[nb][1] = 0.0;
+  for (int nb = KA; nb < KB; ++nb) w[nb][0] = w[nb][1] = 0.0;
   // W^T (8 x IB) += X (8 x rows) * V (rows x IB); B fragments of the next
   // row group are loaded while the current group's DMMAs issue
 #pragma unroll
@@ -175,7 +176,7 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
       for (int gg = 0; gg < 4; ++gg) {
         double bc[2][4];
 #pragma unroll
-        for (int nb = 0; nb < 4; ++nb) {
+        for (int nb = KA; nb < KB; ++nb) {
           const double* vb = Vs + ((rb * 4 + gg) * (IB / 8) + nb) * 64;
           bc[0][nb] = vb[s1a];
           bc[1][nb] = vb[s1b];
@@ -184,16 +185,16 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int nb = 0; nb < 4; ++nb)
+          for (int nb = KA; nb < KB; ++nb)
             if (!(dg && zero_blk(gg, nb))) dmma(w[nb], x[rb * 4 + gg][h], bc[h][nb]);
         pf();
       }
     }
-    if (rb == NB / IB / 2 - 1) mid(x);
+    if (rb == NB / IB / 2 - 1) mid(x);  // (a no-op after its first call)
   }
   if (top) {
 #pragma unroll
-    for (int nb = 0; nb < 4; ++nb) {
+    for (int nb = KA; nb < KB; ++nb) {
       w[nb][0] += ap[nb][0];
       w[nb][1] += ap[nb][1];
     }
@@ -201,9 +202,9 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
   // W^T <- W^T T (Q^T) or W^T T^T (Q); T upper triangular
   double tb[2][4][4];
 #pragma unroll
-  for (int kb = 0; kb < 4; ++kb)
+  for (int kb = KA; kb < KB; ++kb)
 #pragma unroll
-    for (int nb = 0; nb < 4; ++nb)
+    for (int nb = KA; nb < KB; ++nb)
       if (TRANST ? (kb <= nb) : (kb >= nb)) {
         const double* tp = TRANST ? Ts + (kb * 4 + nb) * 64 : Ts + (nb * 4 + kb) * 64;
         tb[0][kb][nb] = tp[TRANST ? s1a : s3a];
@@ -211,20 +212,20 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
       }
   double wt[4][2];
 #pragma unroll
-  for (int nb = 0; nb < 4; ++nb) wt[nb][0] = wt[nb][1] = 0.0;
+  for (int nb = KA; nb < KB; ++nb) wt[nb][0] = wt[nb][1] = 0.0;
 #pragma unroll
-  for (int kb = 0; kb < 4; ++kb)
+  for (int kb = KA; kb < KB; ++kb)
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int nb = 0; nb < 4; ++nb)
+      for (int nb = KA; nb < KB; ++nb)
         if (TRANST ? (kb <= nb) : (kb >= nb)) dmma(wt[nb], w[kb][h], tb[h][kb][nb]);
   if (top) {
 #pragma unroll
-    for (int nb = 0; nb < 4; ++nb) stcg2(top + 8 * nb + 2 * c + r * NB, ap[nb][0] - wt[nb][0], ap[nb][1] - wt[nb][1]);
+    for (int nb = KA; nb < KB; ++nb) stcg2(top + 8 * nb + 2 * c + r * NB, ap[nb][0] - wt[nb][0], ap[nb][1] - wt[nb][1]);
   }
 #pragma unroll
-  for (int nb = 0; nb < 4; ++nb) {
+  for (int nb = KA; nb < KB; ++nb) {
     wt[nb][0] = -wt[nb][0];
     wt[nb][1] = -wt[nb][1];
   }
@@ -238,7 +239,7 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
 #pragma unroll
       for (int gg = 0; gg < 4; ++gg) acc3[gg][0] = acc3[gg][1] = 0.0;
 #pragma unroll
-      for (int kb = 0; kb < 4; ++kb) {
+      for (int kb = KA; kb < KB; ++kb) {
         double bc[2][4];
 #pragma unroll
         for (int gg = 0; gg < 4; ++gg) {
@@ -267,8 +268,36 @@ __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int 
 #endif
     }
   }
-  pf.flush();
   UPROF_MARK_V(12, _tq);
+}
+
+// Apply the staged ib-block reflector (see warp_apply_k).  SPLIT (off: measured
+// 2-5 % slower, the halves serialize through X): as two
+// 16-reflector halves, (I - V2 T22 V2^T)(I - V1 T11 V1^T) for Q^T (reverse
+// for Q) — the same transformation; the T multiply then costs 12 instead of
+// 20 DMMAs per warp (T12 is not needed).
+#ifndef TQR_SPLIT_T
+#define TQR_SPLIT_T 0
+#endif
+template <int NB, bool TRANST, int TRI = 2, int RBL = 0, int RBH = NB / IB, class PF = NoPf, class MID = NoMid,
+          bool SPLIT = (TQR_SPLIT_T != 0)>
+__device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int rb1, const double* __restrict__ Vs,
+                                           const double* __restrict__ Ts, double* top, int lane,
+                                           const double* top_s = nullptr, int drb = -1, PF pf = PF(),
+                                           MID mid = MID()) {
+  if constexpr (!SPLIT) {
+    warp_apply_k<NB, TRANST, TRI, RBL, RBH, 0, 4>(x, rb0, rb1, Vs, Ts, top, lane, top_s, drb, pf, mid);
+  } else {
+    NoMid none;
+    if constexpr (TRANST) {
+      warp_apply_k<NB, TRANST, TRI, RBL, RBH, 0, 2>(x, rb0, rb1, Vs, Ts, top, lane, top_s, drb, pf, mid);
+      warp_apply_k<NB, TRANST, TRI, RBL, RBH, 2, 4>(x, rb0, rb1, Vs, Ts, top, lane, top_s, drb, pf, none);
+    } else {
+      warp_apply_k<NB, TRANST, TRI, RBL, RBH, 2, 4>(x, rb0, rb1, Vs, Ts, top, lane, top_s, drb, pf, mid);
+      warp_apply_k<NB, TRANST, TRI, RBL, RBH, 0, 2>(x, rb0, rb1, Vs, Ts, top, lane, top_s, drb, pf, none);
+    }
+  }
+  pf.flush();
 }
 
 // x rows [8*g0, 8*g1) of the warp's columns (column-major tile, ld NB)

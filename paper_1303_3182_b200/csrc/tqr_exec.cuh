@@ -182,6 +182,7 @@ template <int NB, bool TRANST>
 __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_cur, s_nxt;
+  __shared__ int s_ready;  // item whose predecessors the producer already acquired (or -1)
   __shared__ __align__(8) unsigned long long bars[4];  // full[2], empty[2]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // each CTA holds one dequeued item ahead (deadlock-free: items are taken in
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
     mbar_init(&bars[3], NW);
     s_cur = atomicAdd(P.queue, 1);
     s_nxt = s_cur < P.n_items ? atomicAdd(P.queue, 1) : P.n_items;
+    s_ready = -1;
   }
   bar_all();
   unsigned seq = 0;
@@ -251,6 +253,9 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
             }
             if (ok) __threadfence();  // drop stale L1 lines before cp.async.ca reads
             s_early = ok;
+            // the consumers may skip their own check of nx (read after the
+            // item-finished barrier, which orders this acquire before them)
+            s_ready = ok ? nx : -1;
             if (P.trace) atomicAdd(P.trace + 4 * size_t(P.n_items) + 56 + (ok ? 0 : 1), 1ull);
           }
           asm volatile("bar.sync 2, 128;\n" ::: "memory");
@@ -280,15 +285,17 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
     const Item I = P.items[it];
     unsigned long long t_deq = 0;
     if (P.trace && tid == 0) t_deq = gtimer();
-    if (warp == 0) {
-      for (int t = lane; t < I.pred_n; t += 32) {
-        const int pr = P.preds[I.pred_lo + t];
-        while (ld_acquire(P.done + pr) == 0) __nanosleep(40);
+    if (s_ready != it) {
+      if (warp == 0) {
+        for (int t = lane; t < I.pred_n; t += 32) {
+          const int pr = P.preds[I.pred_lo + t];
+          while (ld_acquire(P.done + pr) == 0) __nanosleep(40);
+        }
+        __syncwarp();
+        __threadfence();  // gpu-scope fence: also drops stale L1 lines
       }
-      __syncwarp();
-      __threadfence();  // gpu-scope fence: also drops stale L1 lines
+      csync();  // dependencies satisfied (the producer checks them itself)
     }
-    csync();  // dependencies satisfied (the producer checks them itself)
     unsigned long long t_rdy = 0;
     if (P.trace && tid == 0) t_rdy = gtimer();
     unsigned long long* pprof = P.trace ? P.trace + 4 * size_t(P.n_items) : nullptr;

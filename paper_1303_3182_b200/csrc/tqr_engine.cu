@@ -177,16 +177,15 @@ void expand(const std::vector<Task>& tasks, const std::vector<std::vector<int32_
   }
 }
 
-// Device-realistic relative cost of one work item (an update slab = 1).
-// Overridable for tuning: TQR_COST_PANEL (GEQRT/TTQRT at nb=256),
-// TQR_COST_PACK, TQR_COST_UNPACK.
+// Relative cost of one work item for the list schedule (an update slab = 1).
+// Overridable for tuning: TQR_COST_PANEL (GEQRT at nb=256), TQR_COST_PACK,
+// TQR_COST_UNPACK.
 double env_cost(const char* k, double dflt) {
   const char* v = getenv(k);
   return v ? atof(v) : dflt;
 }
-inline double item_cost(int kind, int nb) {
-  static const double panel = env_cost("TQR_COST_PANEL", 3.5), pack = env_cost("TQR_COST_PACK", 0.1),
-                      unpack = env_cost("TQR_COST_UNPACK", 0.5);
+inline double item_cost(int kind, int nb, double panel) {
+  static const double pack = env_cost("TQR_COST_PACK", 0.1), unpack = env_cost("TQR_COST_UNPACK", 0.5);
   const double big = nb >= 256 ? 1.0 : 0.5;
   switch (kind) {
     case tqr::PACK: return pack;
@@ -220,7 +219,14 @@ void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers
       succ[size_t(fill[size_t(u)]++)] = int32_t(v);
     }
   std::vector<double> w(n), prio(n, 0.0);
-  for (size_t v = 0; v < n; ++v) w[v] = item_cost(items[v].kind, nb);
+  // panel weight: with plenty of update work per SM (C3: ~4700 slab items)
+  // a light panel weight lets updates fill the machine (measured best 3.0);
+  // with little (C4: ~160) the panels' critical path dominates and a heavy
+  // weight that starts them early is best (measured plateau 8-20)
+  size_t n_upd = 0;
+  for (size_t v = 0; v < n; ++v) n_upd += (items[v].kind >= tqr::UNMQR && items[v].kind <= tqr::TSMQR);
+  const double panel = env_cost("TQR_COST_PANEL", n_upd >= 2000 * size_t(workers) ? 3.0 : 10.0);
+  for (size_t v = 0; v < n; ++v) w[v] = item_cost(items[v].kind, nb, panel);
   // simulated durations: the panel cost may differ from the one the
   // priorities use (TQR_SIM_PANEL: panel items' duration multiplier)
   static const double sim_panel = env_cost("TQR_SIM_PANEL", 1.0);

@@ -376,7 +376,8 @@ int g_wait32(cudaStream_t s, int* addr, unsigned v) {  // CU_STREAM_WAIT_VALUE_G
   return g_wt32(s, reinterpret_cast<unsigned long long>(addr), v, 0);
 }  // tqr_set_trace: per-item timestamps of the next run
 
-// debug knobs from the environment: TQR_GRID (CTAs), TQR_FLAGS (bit 0: no early staging)
+// debug knobs from the environment: TQR_GRID (CTAs), TQR_FLAGS (bit 0: no early
+// staging, bit 1: no L2 prefetch of the next item)
 int env_int(const char* k, int dflt) {
   const char* v = getenv(k);
   return v ? atoi(v) : dflt;

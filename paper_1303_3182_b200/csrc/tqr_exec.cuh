@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
     for (;;) {
       if (it >= P.n_items) break;
       const Item I = P.items[it];
-      if (warp == NW && lane == 0 && nx < P.n_items) prefetch_item<NB>(P, P.items[nx]);
+      if (warp == NW && lane == 0 && nx < P.n_items && !(P.flags & 2)) prefetch_item<NB>(P, P.items[nx]);
       const bool upd = is_update_kind(I.kind);
       if (upd) {
         if (!pre) {

@@ -14,8 +14,10 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-BUILD = os.path.join(ROOT, "build")
-OUT = os.path.join(HERE, "libtqr.so")
+# TQR_BUILD_DIR / TQR_LIB_OUT: separate object dir and output for instrumented
+# builds (TQR_EXTRA_NVCC_FLAGS), so they never mix with the product library
+BUILD = os.environ.get("TQR_BUILD_DIR") or os.path.join(ROOT, "build")
+OUT = os.environ.get("TQR_LIB_OUT") or os.path.join(HERE, "libtqr.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXXFLAGS = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "-I", os.path.join(ROOT, "include")]

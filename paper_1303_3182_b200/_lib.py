@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtqr.so")
+# TQR_LIB_PATH: an instrumented build (tools/, profiling only)
+LIB_PATH = os.environ.get("TQR_LIB_PATH") or os.path.join(HERE, "libtqr.so")
 
 TQR_OK, TQR_EVALUE, TQR_EKEY, TQR_EASSERT, TQR_EOTHER, TQR_ECUDA = 0, -1, -2, -3, -4, -5
 TQR_NO_BS = -(2 ** 31)

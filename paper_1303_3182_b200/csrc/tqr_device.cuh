@@ -24,7 +24,7 @@
 namespace tqrk {
 
 #ifdef TQR_PROF_UPD
-__device__ unsigned long long g_uprof[16];
+__device__ unsigned long long g_uprof[32];
 #define UPROF_MARK(k) UPROF_MARK_V(k, _tp)
 #define UPROF_MARK_V(k, v)                                                    \
   do {                                                                        \
@@ -122,8 +122,13 @@ enum Mode : int { GE = 0, TT = 1, TS = 2 };
 //   Q  : same with W = T W                                  (TRANST = false)
 // The row loop is unrolled per 32-row block (4 DMMA row groups) so the
 // B-fragment loads of a block are scheduled ahead of its DMMAs.
+// pf(x, idx) runs after every 8-row group of the first GEMM (idx = 4 rb +
+// gg) and after every reflector quarter of the second (idx = 32 + 4 rb +
+// kb); idx folds to a constant once the loops are unrolled, so a schedule
+// can move X loads / stores between the DMMAs (XSched below).
 struct NoPf {
-  __device__ __forceinline__ void operator()() const {}
+  template <class X>
+  __device__ __forceinline__ void operator()(X&, int) const {}
   __device__ __forceinline__ void flush() const {}
 };
 
@@ -187,7 +192,7 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
 #pragma unroll
           for (int nb = KA; nb < KB; ++nb)
             if (!(dg && zero_blk(gg, nb))) dmma(w[nb], x[rb * 4 + gg][h], bc[h][nb]);
-        pf();
+        pf(x, rb * 4 + gg);
       }
     }
     if (rb == NB / IB / 2 - 1) mid(x);  // (a no-op after its first call)
@@ -257,7 +262,7 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
 #else
             if (!(dg && zero_blk(gg, kb))) dmma(acc3[gg], wt[kb][h], bc[h][gg]);
 #endif
-        pf();
+        pf(x, 32 + rb * 4 + kb);
       }
 #ifndef TQR_DIRECT_ACC
 #pragma unroll
@@ -323,6 +328,56 @@ __device__ __forceinline__ void store_x(const double (&x)[NB / 8][2], double* co
   for (int g = 0; g < NB / 8; ++g)
     if (g >= g0 && g < g1) stcg2(col + r * NB + 8 * g + 2 * c, x[g][0], x[g][1]);
 }
+
+// X traffic spread over one reflector block's DMMA stream (pf hook of
+// warp_apply): a burst of 16 loads / stores per lane at a block boundary
+// stalls both warps of an SMSP on the LSU queue for thousands of cycles;
+// one or two row groups per call overlap it with the DMMAs.
+//   XS_TT_LOAD   (TT block 0, rows < IB): load the lower half, 2 groups per
+//                call over the 4 + 4 calls of the block
+//   XS_GE_LOAD   (GE block 0): load the lower half, one group per call of
+//                the first GEMM's upper-half row groups
+//   XS_GE_STORE  (GE block NBLK/2): store the final upper half, one group per
+//                call of the first GEMM (rows >= NB/2 only)
+//   XS_GE_STORE2 (GE last block, NB > 64): store rows NB/2 .. NB-33 (final
+//                after the block before), 3 groups per first-GEMM call
+enum XsKind : int { XS_TT_LOAD, XS_GE_LOAD, XS_GE_STORE, XS_GE_STORE2 };
+template <int NB, int KIND>
+struct XSched {
+  double* col;  // the warp's 8 columns (column-major tile, ld NB)
+  int lane;
+  template <class X>
+  __device__ __forceinline__ void operator()(X& x, int idx) const {
+    constexpr int G = NB / 8, GH = NB / 16, NBLK = NB / IB;
+    const int r = lane >> 2, c = lane & 3;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      bool hit = false;
+      if (KIND == XS_TT_LOAD) {
+        const int call = idx < 32 ? idx : 4 + (idx - 32);  // 0..7
+        constexpr int per = (G - GH + 7) / 8;
+        hit = g >= GH && idx < 36 && (idx < 4 || idx >= 32) && (g - GH) / per == call;
+      } else if (KIND == XS_GE_LOAD) {
+        hit = g >= GH && idx < GH && g - GH == idx;
+      } else if (KIND == XS_GE_STORE) {
+        hit = g < GH && idx >= GH && idx < 2 * GH && g == idx - GH;
+      } else {
+        constexpr int first = 4 * (NBLK - 1), n = G - 4 - GH, per = n > 0 ? (n + 3) / 4 : 1;
+        hit = n > 0 && g >= GH && g < G - 4 && idx >= first && idx < first + 4 && (g - GH) / per == idx - first;
+      }
+      if (hit) {
+        if (KIND == XS_TT_LOAD || KIND == XS_GE_LOAD) {
+          double2 v = ldcg2(col + r * NB + 8 * g + 2 * c);
+          x[g][0] = v.x;
+          x[g][1] = v.y;
+        } else {
+          stcg2(col + r * NB + 8 * g + 2 * c, x[g][0], x[g][1]);
+        }
+      }
+    }
+  }
+  __device__ __forceinline__ void flush() const {}
+};
 
 __device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));

@@ -74,9 +74,12 @@ __device__ void update_produce(double* sm, const double* __restrict__ vt, const 
   using S = Smem<NB>;
   constexpr int NBLK = NB / IB;
   const int scol0 = slab * WS;
+  UPROF_DECL_V(_pp);
   for (int s = s_begin; s < s_end; ++s) {
     const unsigned q = seq + unsigned(s), buf = q & 1u;
+    UPROF_MARK_V(5, _pp);
     if (q >= 2) mbar_wait(&empty[buf], ((q >> 1) - 1u) & 1u);
+    UPROF_MARK_V(3, _pp);
     const int b = TRANST ? s : NBLK - 1 - s;
     int r0, r1;
     upd_rows<NB, MODE>(b, r0, r1);
@@ -85,6 +88,7 @@ __device__ void update_produce(double* sm, const double* __restrict__ vt, const 
     if (MODE != GE) pstage_top<NB>(sm + (buf ? S::U_P1 : S::U_P0), topt, scol0, b * IB, pw, lane);
     mbar_arrive_cpasync(&full[buf]);  // completion of this thread's copies
     mbar_arrive(&full[buf]);          // release of its direct stores
+    UPROF_MARK_V(4, _pp);
   }
 }
 
@@ -101,21 +105,21 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
   double* const xc = xt + size_t(col0) * NB;
   double x[NB / 8][2];
   // one reflector block: wait for its staged V/T, apply, release the buffer
-  auto block = [&](int s, auto rbl, auto rbh, auto mid) {
+  auto block = [&](int s, auto rbl, auto rbh, auto pf) {
     const unsigned q = seq + unsigned(s), buf = q & 1u;
     const int b = TRANST ? s : NBLK - 1 - s;
 #ifndef TQR_ABL_NOPROD
     mbar_wait(&full[buf], (q >> 1) & 1u);
 #endif
-    UPROF_MARK(0);
+    UPROF_MARK((MODE == GE ? 16 : 24) + s);
     int r0, r1;
     upd_rows<NB, MODE>(b, r0, r1);
     const double* Vs = sm + (buf ? S::U_V1 : S::U_V0);
     const double* Ts = sm + (buf ? S::U_T1 : S::U_T0);
     double* top = (MODE == GE) ? nullptr : topt + size_t(col0) * NB + b * IB;
     const double* top_s = (MODE == GE) ? nullptr : sm + (buf ? S::U_P1 : S::U_P0) + warp * 8 * TLD;
-    warp_apply<NB, TRANST, MODE, decltype(rbl)::value, decltype(rbh)::value>(x, r0 / IB, r1 / IB, Vs, Ts, top, lane,
-                                                                             top_s, b, NoPf(), mid);
+    warp_apply<NB, TRANST, MODE, decltype(rbl)::value, decltype(rbh)::value, decltype(pf)>(
+        x, r0 / IB, r1 / IB, Vs, Ts, top, lane, top_s, b, pf);
     __syncwarp();
 #ifndef TQR_ABL_NOPROD
     if (lane == 0) mbar_arrive(&empty[buf]);
@@ -126,35 +130,36 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
   using RH = std::integral_constant<int, NBLK / 2>;
   using RN = std::integral_constant<int, NBLK>;
   constexpr int GH = NB / 16;  // x row groups of the upper half
-  // loads of one half of X are issued only after the first use of the other
-  // half (all loads in flight share one scoreboard, so the first DMMA would
-  // otherwise wait for every one of them)
-  auto load_lower = [&](auto&) { load_x<NB, false>(x, xc, GH, NB / 8, lane); };
   if constexpr (TRANST && MODE == TT) {
     // Q^T with an upper-triangular V: block b only reads x rows of blocks
-    // <= b, so the lower half of X loads while the first blocks run
+    // <= b, so the lower half of X loads during block 0's DMMAs
     load_x<NB, false>(x, xc, 0, GH, lane);
     UPROF_MARK(8);
-    block(0, R0{}, RH{}, NoMid());
-    load_lower(x);
-    for (int s = 1; s < NBLK / 2; ++s) block(s, R0{}, RH{}, NoMid());
-    for (int s = NBLK / 2; s < NBLK; ++s) block(s, R0{}, RN{}, NoMid());
+    block(0, R0{}, RH{}, XSched<NB, XS_TT_LOAD>{xc, lane});
+    for (int s = 1; s < NBLK / 2; ++s) block(s, R0{}, RH{}, NoPf());
+    for (int s = NBLK / 2; s < NBLK; ++s) block(s, R0{}, RN{}, NoPf());
     store_x<NB>(x, xc, 0, NB / 8, lane);
   } else if constexpr (TRANST && MODE == GE) {
-    // Q^T with a unit-lower V: the lower half of X loads while block 0 works
-    // on the upper half; rows of blocks < b are final once block b starts,
-    // so the upper half is stored while blocks >= NBLK/2 run
+    // Q^T with a unit-lower V: the lower half of X loads during block 0's
+    // first GEMM on the upper half; rows of blocks < b are final once block b
+    // starts, so the upper half is stored during block NBLK/2 and the rows
+    // up to the last block during the last block
     load_x<NB, false>(x, xc, 0, GH, lane);
     UPROF_MARK(8);
-    block(0, R0{}, RN{}, load_lower);
-    for (int s = 1; s < NBLK / 2; ++s) block(s, R0{}, RN{}, NoMid());
-    store_x<NB>(x, xc, 0, GH, lane);
-    for (int s = NBLK / 2; s < NBLK; ++s) block(s, RH{}, RN{}, NoMid());
-    store_x<NB>(x, xc, GH, NB / 8, lane);
+    block(0, R0{}, RN{}, XSched<NB, XS_GE_LOAD>{xc, lane});
+    for (int s = 1; s < NBLK / 2; ++s) block(s, R0{}, RN{}, NoPf());
+    block(NBLK / 2, RH{}, RN{}, XSched<NB, XS_GE_STORE>{xc, lane});
+    if constexpr (NBLK / 2 < NBLK - 1) {
+      for (int s = NBLK / 2 + 1; s < NBLK - 1; ++s) block(s, RH{}, RN{}, NoPf());
+      block(NBLK - 1, RH{}, RN{}, XSched<NB, XS_GE_STORE2>{xc, lane});
+      store_x<NB>(x, xc, NB / 8 - 4, NB / 8, lane);
+    } else {
+      store_x<NB>(x, xc, GH, NB / 8, lane);
+    }
   } else {
     load_x<NB>(x, xc, 0, NB / 8, lane);
     UPROF_MARK(8);
-    for (int s = 0; s < NBLK; ++s) block(s, R0{}, RN{}, NoMid());
+    for (int s = 0; s < NBLK; ++s) block(s, R0{}, RN{}, NoPf());
     store_x<NB>(x, xc, 0, NB / 8, lane);
   }
   UPROF_MARK(6);

@@ -85,13 +85,18 @@ void run(const char* name, int sms) {
   const double dmma_flops = double(dm) * 8 * 512 * sms * reps;
   const double useful = 2.0 * NB * NB * WS * (MODE == TS ? 2.0 : 1.0) * sms * reps;
 #ifdef TQR_PROF_UPD
-  unsigned long long hp[16];
+  unsigned long long hp[32];
   cudaMemcpyFromSymbol(hp, g_uprof, sizeof(hp));
-  unsigned long long zero[16] = {0};
+  unsigned long long zero[32] = {0};
   cudaMemcpyToSymbol(g_uprof, zero, sizeof(zero));
+  for (int i = 16; i < 32; ++i) hp[0] += hp[i];
   double tot = double(hp[0] + hp[2] + hp[6] + hp[8]);
   printf("phases (frac): load_x %.3f wait_full %.3f apply %.3f [gemm1 %.3f T %.3f gemm3 %.3f] store %.3f\n",
          hp[8] / tot, hp[0] / tot, hp[2] / tot, hp[10] / tot, hp[11] / tot, hp[12] / tot, hp[6] / tot);
+  printf("producer per warp-item: wait empty %.0f issue %.0f\n", hp[3] / (4.0 * 148 * 68), hp[4] / (4.0 * 148 * 68));
+  printf("wait_full per block:");
+  for (int i = 0; i < 8; ++i) printf(" %.0f", (hp[16 + i] + hp[24 + i]) / (8.0 * 148 * 68));
+  printf("\n");
 #endif
   printf("{\"item\": \"%s\", \"nb\": %d, \"us_per_item\": %.2f, \"dmma_tflops\": %.2f, \"useful_tflops\": %.2f, \"err\": \"%s\"}\n",
          name, NB, us, dmma_flops / (ms * 1e-3) / 1e12, useful / (ms * 1e-3) / 1e12,

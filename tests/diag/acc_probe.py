@@ -3,7 +3,7 @@ for small tile grids (one GEQRT; one TT elimination; 4x4 tiles)."""
 import os, sys
 import numpy as np
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_1303_3182_b200 as P
 from paper_1303_3182_b200.engine import tiled_qr
 from oracle.replay import replay_build

@@ -2,7 +2,7 @@
 Greedy trace at reduced and full size, on the CPU (reference numbers)."""
 import os, sys, time
 import numpy as np
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_1303_3182_b200 as P
 from oracle.replay import replay_build
 

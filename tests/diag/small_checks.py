@@ -7,7 +7,7 @@ import sys
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from oracle.replay import row_sign_normalize  # noqa: E402
 from paper_1303_3182_b200.engine import tiled_qr, tiled_qr_host  # noqa: E402
 

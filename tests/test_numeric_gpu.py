@@ -180,7 +180,7 @@ def test_more_trees_nb256_vs_replay(algo, family, bs, p, q):
 
 
 # ||Q^T Q - I||_F of the LAPACK replay (oracle/replay.py) of the same C3
-# Greedy trace, measured on the GPU box's CPU (tools/replay_orth.py,
+# Greedy trace, measured on the GPU box's CPU (tests/diag/replay_orth.py,
 # profiles/accuracy_r01.json): the reference algorithm itself lands just
 # above 1e-12 at n = 16384, so the bar there is "within 1.5x of the replay".
 REPLAY_ORTH = {8192: 5.077e-13, 16384: 1.018e-12}

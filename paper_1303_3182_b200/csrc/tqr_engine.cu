@@ -29,6 +29,7 @@ using namespace tqrk;
 using namespace tqrx;
 namespace tqrx {
 int g_flags = 0;
+int g_carveout = -1;
 }
 
 namespace {
@@ -398,6 +399,7 @@ cudaError_t run(const DevSched& d, int nb, bool transT, const double* vtiles, do
   if (d.n_items == 0) return cudaSuccess;
   DevView v{d.items, d.preds, d.done, d.queue, d.n_items};
   tqrx::g_flags = env_int("TQR_FLAGS", 0);
+  tqrx::g_carveout = env_int("TQR_CARVEOUT", -1);
   const int grid = std::min(d.n_items, std::max(1, env_int("TQR_GRID", num_sms())));
   switch (nb) {
     case 64:

@@ -354,6 +354,7 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
 }
 
 extern int g_flags;
+extern int g_carveout;  // debug: TQR_CARVEOUT (percent of the unified L1/smem for shared memory)
 
 struct IoBufs {
   const double* a_src = nullptr;
@@ -396,6 +397,10 @@ TQR_DECLARE_LAUNCH(256, false)
     const size_t smem = Smem<NB>::BYTES;                                                                           \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));            \
     if (e != cudaSuccess) return e;                                                                                \
+    if (g_carveout >= 0) {                                                                                         \
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout);                 \
+      if (e != cudaSuccess) return e;                                                                              \
+    }                                                                                                              \
     ExecParams P{d.items,  d.preds, d.n_items, d.done,  d.queue,  vtiles,   tiles, tg,                              \
                  te,       p,       trace,     g_flags, io.a_src, io.lda, io.arrive, io.r_dst, io.ldr, io.r_ready, io.acr, io.anch};           \
     kern<<<grid, NTP, smem, st>>>(P);                                                                               \

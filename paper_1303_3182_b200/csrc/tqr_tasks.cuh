@@ -8,25 +8,30 @@
 
 namespace tqrk {
 
-// Shared-memory carve-up (doubles).  Update items: Vs[2] + Ts[2] + pivot rows[2].
-// Panel items: top block, staged V/T for the trailing update, Gram column
-// store, reduction partials, diagonal-row / s broadcasts, per-column scalars.
+// Shared-memory carve-up (doubles), kept small: what is left of the
+// unified 256 KB L1/shared memory is L1, which the 8-byte cp.async staging of
+// reflector blocks relies on (forcing the largest carveout costs 4 % at C3).
+// Update items: Vs[2] + Ts[2] (the pivot rows of TT/TS items are read from
+// global memory, in flight during the first GEMM).  Panel items: the stacked
+// panel P, Ts, then a region shared by the factorization scratch (Gram, T,
+// group-update partials, per-column scalars) and the staged V of the
+// trailing update (written after T is staged, dead before the next block).
 template <int NB>
 struct Smem {
   static constexpr int VS = NB * IB;  // one staged V block
   static constexpr int TS = IB * IB;
   // update layout
-  static constexpr int TOP = TLD * WS;  // staged pivot rows of a slab (TT/TS)
-  static constexpr int U_V0 = 0, U_V1 = VS, U_T0 = 2 * VS, U_T1 = 2 * VS + TS, U_P0 = 2 * VS + 2 * TS,
-                       U_P1 = U_P0 + TOP, U_END = U_P1 + TOP;
-  // panel layout: stacked panel P (column-major, ld PLD = 4 mod 16), staged
-  // V/T for the trailing update, Gram, T, group-update partials and scalars
+  static constexpr int U_V0 = 0, U_V1 = VS, U_T0 = 2 * VS, U_T1 = 2 * VS + TS, U_END = 2 * VS + 2 * TS;
+  // panel layout: stacked panel P (column-major, ld PLD = 4 mod 16)
   static constexpr int PLD = NB + IB + 4;
   static constexpr int LDW = IB + 4;
-  static constexpr int P_P = 0, P_V = P_P + PLD * IB, P_T = P_V + VS, P_G = P_T + TS, P_TT = P_G + TS;
+  static constexpr int P_P = 0, P_T = P_P + PLD * IB, P_X = P_T + TS;
+  static constexpr int P_V = P_X;  // aliases everything below
+  static constexpr int P_G = P_X, P_TT = P_G + TS;
   static constexpr int P_WP = P_TT + TS, P_W = P_WP + NW * 8 * LDW, P_TG = P_W + 8 * LDW;
   static constexpr int P_PART = P_TG + 64, P_DROW = P_PART + 2 * NW * 8, P_SBUF = P_DROW + 16, P_SC = P_SBUF + 8;
-  static constexpr int P_END = P_SC + 3 * IB + 8;
+  static constexpr int P_SCR_END = P_SC + 3 * IB + 8;
+  static constexpr int P_END = (P_V + VS > P_SCR_END) ? P_V + VS : P_SCR_END;
   static constexpr int END = U_END > P_END ? U_END : P_END;
   static constexpr size_t BYTES = size_t(END) * sizeof(double);
 };
@@ -85,7 +90,6 @@ __device__ void update_produce(double* sm, const double* __restrict__ vt, const 
     upd_rows<NB, MODE>(b, r0, r1);
     pstage_v<NB, MODE>(sm + (buf ? S::U_V1 : S::U_V0), vt, b, r0, r1, pw, lane);
     pstage_t(sm + (buf ? S::U_T1 : S::U_T0), tt, b, pw, lane);
-    if (MODE != GE) pstage_top<NB>(sm + (buf ? S::U_P1 : S::U_P0), topt, scol0, b * IB, pw, lane);
     mbar_arrive_cpasync(&full[buf]);  // completion of this thread's copies
     mbar_arrive(&full[buf]);          // release of its direct stores
     UPROF_MARK_V(4, _pp);
@@ -117,7 +121,7 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
     const double* Vs = sm + (buf ? S::U_V1 : S::U_V0);
     const double* Ts = sm + (buf ? S::U_T1 : S::U_T0);
     double* top = (MODE == GE) ? nullptr : topt + size_t(col0) * NB + b * IB;
-    const double* top_s = (MODE == GE) ? nullptr : sm + (buf ? S::U_P1 : S::U_P0) + warp * 8 * TLD;
+    const double* top_s = nullptr;  // pivot rows straight from global memory
     warp_apply<NB, TRANST, MODE, decltype(rbl)::value, decltype(rbh)::value, decltype(pf)>(
         x, r0 / IB, r1 / IB, Vs, Ts, top, lane, top_s, b, pf);
     __syncwarp();
@@ -632,6 +636,7 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
       Ts[swz(i, j)] = v;
       tslot[i + size_t(rb0 + j) * IB] = v;
     }
+    csync();  // Vs overwrites Tp / G / the scalars
     if (MODE == GE) {
       for (int e = tid; e < nrows * IB; e += NT) {
         const int r = e % nrows, c = e / nrows;

@@ -72,13 +72,15 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 }
 
 // in-sub-block swizzle: element (a, b) (row, col) of an 8x8 sub-block ->
-// 0..63 such that the DMMA B-fragment reads of lane (r, c), {(2c+h, r)}
-// (W = V^T X) and {(r, 2c+h)} (X -= W V^T), each hit 16 distinct 8-byte
-// banks per half-warp.
+// 0..63.  Rows 2k, 2k+1 of a column are adjacent (16-byte staging copies of
+// a column's row pair; one 16-byte load gives the B fragments (2c, r) and
+// (2c+1, r) of both k-halves of W = V^T X), and both fragment patterns hit
+// distinct banks: (2c+h, r) as 16-byte loads per quarter-warp, (r, 2c+h)
+// (X -= W V^T) as 8-byte loads per half-warp.
 __device__ __forceinline__ int swz_in(int a, int b) {
   const int a0 = a & 1, a1 = (a >> 1) & 1, a2 = (a >> 2) & 1;
   const int b0 = b & 1, b1 = (b >> 1) & 1, b2 = (b >> 2) & 1;
-  return (a0 << 5) | (b2 << 4) | (a1 << 3) | (b1 << 2) | ((a2 ^ a0) << 1) | (b0 ^ b2);
+  return a0 | (a1 << 1) | ((a2 ^ b1) << 2) | ((b0 ^ b2) << 3) | (b1 << 4) | (b2 << 5);
 }
 // element (row, col) of a [rows x IB] block
 __device__ __forceinline__ int swz(int row, int col) { return ((row >> 3) * (IB / 8) + (col >> 3)) * 64 + swz_in(row & 7, col & 7); }
@@ -153,7 +155,7 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
   // is V sub-block (row group gg, column group cb) of the diagonal block zero?
   auto zero_blk = [](int gg, int cb) { return TRI == 0 ? (gg < cb) : (TRI == 1 ? (gg > cb) : false); };
   const int r = lane >> 2, c = lane & 3;
-  const int s1a = swz_in(2 * c, r), s1b = swz_in(2 * c + 1, r);  // (2c+h, r)
+  const int s1a = swz_in(2 * c, r);  // (2c+h, r) at s1a + h
   const int s3a = swz_in(r, 2 * c), s3b = swz_in(r, 2 * c + 1);  // (r, 2c+h)
   // top_s: the block's IB pivot rows of this warp's 8 columns staged in smem
   // (column-major, ld TLD); else read from global
@@ -182,9 +184,9 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
         double bc[2][4];
 #pragma unroll
         for (int nb = KA; nb < KB; ++nb) {
-          const double* vb = Vs + ((rb * 4 + gg) * (IB / 8) + nb) * 64;
-          bc[0][nb] = vb[s1a];
-          bc[1][nb] = vb[s1b];
+          const double2 v2 = *reinterpret_cast<const double2*>(Vs + ((rb * 4 + gg) * (IB / 8) + nb) * 64 + s1a);
+          bc[0][nb] = v2.x;
+          bc[1][nb] = v2.y;
         }
         const bool dg = (TRI != 2) && rb == drb;
 #pragma unroll
@@ -212,8 +214,14 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
     for (int nb = KA; nb < KB; ++nb)
       if (TRANST ? (kb <= nb) : (kb >= nb)) {
         const double* tp = TRANST ? Ts + (kb * 4 + nb) * 64 : Ts + (nb * 4 + kb) * 64;
-        tb[0][kb][nb] = tp[TRANST ? s1a : s3a];
-        tb[1][kb][nb] = tp[TRANST ? s1b : s3b];
+        if (TRANST) {
+          const double2 v2 = *reinterpret_cast<const double2*>(tp + s1a);  // s1b == s1a + 1
+          tb[0][kb][nb] = v2.x;
+          tb[1][kb][nb] = v2.y;
+        } else {
+          tb[0][kb][nb] = tp[s3a];
+          tb[1][kb][nb] = tp[s3b];
+        }
       }
   double wt[4][2];
 #pragma unroll
@@ -384,59 +392,51 @@ __device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 
-// Producer staging (the NPW warps of the producer warpgroup, pw = 0..NPW-1).
-// Rows [row0, row1) of reflector block b of tile `vt` (ld NB) into swizzled
-// smem, 8-byte cp.async; one instruction covers 8 rows x 4 columns (16
-// distinct banks per half-warp, 64-byte global segments).  No masking: the
-// diagonal 32x32 block of a GE (unit-lower) / TT (upper) reflector block is
-// masked where the B fragments are read (warp_apply).
+// Producer staging (the NPW warps of the producer warpgroup, pw = 0..NPW-1,
+// warp pw copies columns 8 pw .. 8 pw + 7): rows [row0, row1) of reflector
+// block b of tile `vt` (ld NB) into swizzled smem with 16-byte cp.async.cg
+// (L2 -> smem, no L1 allocation).
 constexpr int NPW = 4;
+static_assert(NPW * 8 == IB, "one 8-column group per producer warp");
 template <int NB, int MODE>
 __device__ __forceinline__ void pstage_v(double* Vs, const double* __restrict__ vt, int b, int row0, int row1, int pw,
                                          int lane) {
-  const int a = lane & 7, cq = lane >> 3;
-  // unit u -> rows row0 + 8*(u>>3) + a, column 4*(u&7) + cq; this warp does
-  // u = pw + NPW*t, i.e. two fixed columns per warp (IB/4 == 2*NPW).  Entries
-  // of the diagonal 32x32 block outside the reflector pattern (GE: unit
-  // lower; TT: upper) are stored directly instead of copied.
-  const int c0 = 4 * pw + cq, c1 = c0 + 4 * NPW;
-  const double* s0 = vt + size_t(b * IB + c0) * NB + a;
-  const double* s1 = vt + size_t(b * IB + c1) * NB + a;
-  double* d0 = Vs + (c0 >> 3) * 64 + swz_in(a, c0 & 7);
-  double* d1 = Vs + (c1 >> 3) * 64 + swz_in(a, c1 & 7);
+  // lane -> row pair p (rows 2p, 2p+1 of each 8-row group), column 8 pw + cq:
+  // one instruction copies 8 rows x 8 columns, 16 bytes per lane (4 lanes
+  // read a column's 64 contiguous bytes).  Entries of the diagonal 32x32
+  // block outside the reflector pattern (GE: unit lower; TT: upper) are
+  // stored directly instead of copied.
+  const int p = lane & 3, cq = lane >> 2;
+  const int c0 = 8 * pw + cq;
+  const double* s0 = vt + size_t(b * IB + c0) * NB + 2 * p;
+  double* d0 = Vs + pw * 64 + swz_in(2 * p, cq);
   const int dg0 = b * IB;
   for (int rr = row0; rr < row1; rr += 8) {
     double* e0 = d0 + (rr >> 3) * (IB / 8) * 64;
-    double* e1 = d1 + (rr >> 3) * (IB / 8) * 64;
-    const int row = rr + a;
     if (MODE == TS || rr < dg0 || rr >= dg0 + IB) {
-      cp_async8(e0, s0 + rr);
-      cp_async8(e1, s1 + rr);
+      cp_async16(e0, s0 + rr);
     } else {
-      const int lr = row - dg0;  // row within the diagonal block
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int cc = h ? c1 : c0;
-        double* e = h ? e1 : e0;
-        const bool live = (MODE == GE) ? (lr > cc) : (lr <= cc);
+        const int lr = rr + 2 * p + h - dg0;  // row within the diagonal block
+        const bool live = (MODE == GE) ? (lr > c0) : (lr <= c0);
         if (live)
-          cp_async8(e, (h ? s1 : s0) + rr);
+          cp_async8(e0 + h, s0 + rr + h);
         else
-          *e = (MODE == GE && lr == cc) ? 1.0 : 0.0;
+          e0[h] = (MODE == GE && lr == c0) ? 1.0 : 0.0;
       }
     }
   }
 }
 
-// T_b (IB x IB; LAPACK ldt = IB, lower part zero as written by the panels)
+// T_b (IB x IB; LAPACK ldt = IB, lower part zero as written by the panels):
+// 16-byte row pairs, 4 per thread
 __device__ __forceinline__ void pstage_t(double* Ts, const double* __restrict__ tt, int b, int pw, int lane) {
-  const int a = lane & 7, cq = lane >> 3;
-  const int c0 = 4 * pw + cq, c1 = c0 + 4 * NPW;
+  const int p = lane & 3, cq = lane >> 2;
+  const int c0 = 8 * pw + cq;
 #pragma unroll
-  for (int rr = 0; rr < IB; rr += 8) {
-    cp_async8(Ts + swz(rr + a, c0), tt + rr + a + size_t(b * IB + c0) * IB);
-    cp_async8(Ts + swz(rr + a, c1), tt + rr + a + size_t(b * IB + c1) * IB);
-  }
+  for (int rr = 0; rr < IB; rr += 8)
+    cp_async16(Ts + swz(rr + 2 * p, c0), tt + rr + 2 * p + size_t(b * IB + c0) * IB);
 }
 
 // IB pivot rows [r0, r0+IB) of WS columns from col0 (ld NB) -> smem,

@@ -6,9 +6,10 @@ tree (coarse_schedule, qr.py:254-297) — no communication.  Then log2(G)
 rounds of binary TT merges: in round s (stride 2^s) rank b = a + stride
 sends its q x q-tile R factor to rank a (one NCCL point-to-point message of
 q*q tiles), and rank a eliminates the stacked [R_a; R_b] column by column
-with TTQRT / TTMQR / GEQRT / UNMQR, pairing rows exactly as Greedy and
-Fibonacci pair them (bottom z live rows against the z rows above,
-qr.py:208-218).  Written as one global elimination list, local trees plus
+with TTQRT / TTMQR / GEQRT / UNMQR, pairing rows as soon as they are ready
+under the device cost model (the Asap event rule, qr.py:551-583; the
+round-1 Greedy-style pairing is kept as merge_pairs_greedy — its critical
+path is 1.8x longer).  Written as one global elimination list, local trees plus
 merges form a valid list under the reference's validate() (qr.py:56-83)
 with unchanged total weight (tests/test_dist.py).
 
@@ -36,11 +37,18 @@ KIND_ID = {k: n for n, k in enumerate(QR_KINDS)}
 # ---------------------------------------------------------------------------
 # schedule side (host, exact)
 
-def merge_pairs(q, row_a, rows_b):
-    """Eliminations merging R_a (rows row_a(k)) with R_b (rows rows_b(i)):
-    per column k the live rows are [row_a(k)] + [rows_b(i) for i <= k];
-    while more than one is live, the bottom z = len//2 are zeroed by the z
-    rows directly above them."""
+# device cost model of the merge pairing (units of ~30 us at nb=256, measured
+# in the executor: TTQRT ~ GEQRT ~ 450 us, one TTMQR tile update ~ 60 us with
+# its four 64-column slabs in parallel)
+MERGE_COST = {"ttqrt": 15, "ttmqr": 2, "geqrt": 15}
+
+
+def merge_pairs_greedy(q, row_a, rows_b):
+    """Greedy-style pairing (round-1 merges, kept for comparison): per column
+    k the live rows are [row_a(k)] + [rows_b(i) for i <= k]; while more than
+    one is live, the bottom z = len//2 are zeroed by the z rows directly
+    above them.  Simulated critical path at q = 8:
+    13.0 ms vs 7.2 ms for merge_pairs."""
     out = []
     for k in range(1, q + 1):
         live = [row_a(k)] + [rows_b(i) for i in range(1, k + 1)]
@@ -51,6 +59,39 @@ def merge_pairs(q, row_a, rows_b):
                 out.append(ElimEntry(t, v, k))
             live = live[:len(live) - z]
     return out
+
+
+def merge_pairs(q, row_a, rows_b, cost=None):
+    """Eliminations merging R_a (rows row_a(k)) with R_b (rows rows_b(i)),
+    paired as soon as possible (the event rule of the reference's Asap,
+    qr.py:551-583, under the device cost model): per column k the live
+    rows are R_a's row k, R_b's row k (both ready at once: untouched by
+    earlier columns) and the rows eliminated in column k-1 (ready after
+    their TTMQR on column k and the GEQRT that re-triangularizes it).  The
+    two earliest-ready rows pair: R_a's row survives when it is one of them
+    (it ends as R's row k), otherwise the lower merge row survives; the
+    survivor is ready again after the TTQRT.  Entries are emitted in
+    simulated start order (ties: row numbers), a valid list order."""
+    import heapq
+
+    c = cost or MERGE_COST
+    ev, carry = [], []
+    for k in range(1, q + 1):
+        live = [(0, k), (0, q + k)] + carry  # (ready time, merge row)
+        carry = []
+        heapq.heapify(live)
+        while len(live) > 1:
+            t1, r1 = heapq.heappop(live)
+            t2, r2 = heapq.heappop(live)
+            s = max(t1, t2)
+            piv, tgt = (r1, r2) if (r1 == k or (r2 != k and r1 < r2)) else (r2, r1)
+            ev.append((s, tgt, piv, k))
+            heapq.heappush(live, (s + c["ttqrt"], piv))
+            carry.append((s + c["ttqrt"] + c["ttmqr"] + c["geqrt"], tgt))
+        assert live[0][1] == k
+    ev.sort()
+    row = lambda r: row_a(r) if r <= q else rows_b(r - q)  # noqa: E731
+    return [ElimEntry(row(t), row(v), k) for _, t, v, k in ev]
 
 
 def composite_list(p, q, G):
@@ -96,19 +137,43 @@ def merge_trace(q):
     return np.asarray(kinds, dtype=np.int8), np.asarray(idx, dtype=np.int32).reshape(-1, 4)
 
 
-def emulate(A, G, nb, backend_cls=None, device=None):
+def emulate(A, G, nb, backend_cls=None, device=None, keep=False):
     """Single-device emulation of tall_skinny_qr with G shards (same local
-    trees and merge order; the exchange is a device copy).  For tests."""
+    trees and merge order; the exchange is a device copy).  For tests.
+    keep=True gives every shard its own backend (the local factors stay for
+    emulate_apply_q) and returns the list of backends."""
     p, q = A.shape[0] // nb, A.shape[1] // nb
     P = p // G
-    be = (backend_cls or GpuBackend)(P, q, nb, device)
+    cls = backend_cls or GpuBackend
+    bes = [cls(P, q, nb, device) for _ in range(G)] if keep else [cls(P, q, nb, device)] * G
     rs = []
     for s in range(G):
-        rs.append(be.factor_local(A[s * P * nb:(s + 1) * P * nb]).clone())
+        rs.append(bes[s].factor_local(A[s * P * nb:(s + 1) * P * nb]).clone())
     for stride, pairs in merge_rounds(G):
         for a, b in pairs:
-            rs[a] = be.merge(rs[a], rs[b]).clone()
-    return be, rs[0]
+            m = bes[a].merge(rs[a], rs[b], key=stride) if keep else bes[a].merge(rs[a], rs[b])
+            rs[a] = m.clone()
+    return (bes if keep else bes[0]), rs[0]
+
+
+def emulate_apply_q(bes, C, trans):
+    """Q^T C (trans) or Q C of an emulate(..., keep=True) factorization; C is
+    the global m x c device matrix, split by the same block rows."""
+    G = len(bes)
+    P, q, nb = bes[0].P, bes[0].q, bes[0].nb
+    cs = [C[s * P * nb:(s + 1) * P * nb].clone() for s in range(G)]
+    h = q * nb
+    rounds = merge_rounds(G)
+    if trans:
+        cs = [be.apply_local(c, True) for be, c in zip(bes, cs)]
+    for stride, pairs in (rounds if trans else rounds[::-1]):
+        for a, b in pairs:
+            ta, tb = bes[a].apply_merge(stride, cs[a][:h], cs[b][:h], trans)
+            cs[a][:h].copy_(ta)
+            cs[b][:h].copy_(tb)
+    if not trans:
+        cs = [be.apply_local(c, False) for be, c in zip(bes, cs)]
+    return cs
 
 
 def merge_rounds(G):
@@ -147,6 +212,7 @@ class GpuBackend:
         self.mtiles, self.mtg, self.mte = self.merge_plan.alloc(device)
         t2 = nb * nb
         self.rbuf = torch.empty(q * q * t2, dtype=torch.float64, device=device)
+        self.merge_factors = {}  # merge key (round stride) -> (tiles, tg, te)
 
     def factor_local(self, A_local):
         self.local_plan.pack(A_local, self.tiles)
@@ -179,15 +245,38 @@ class GpuBackend:
         self.rbuf.view(self.q, self.q * t2).copy_(src)
         return self.rbuf
 
-    def merge(self, r_a, r_b):
-        """[R_a; R_b] -> merged R (q x q tiles, written into r_a)."""
+    def merge(self, r_a, r_b, key=None):
+        """[R_a; R_b] -> merged R (q x q tiles, written into r_a).  With a
+        key the merge's reflectors and T factors are kept for apply_merge."""
         t2 = self.nb * self.nb
         m = self.mtiles.view(self.q, 2 * self.q * t2)
         m[:, :self.q * t2].copy_(r_a.view(self.q, self.q * t2))
         m[:, self.q * t2:].copy_(r_b.view(self.q, self.q * t2))
         self.merge_plan.factor(self.mtiles, self.mtg, self.mte)
+        if key is not None:
+            self.merge_factors[key] = (self.mtiles.clone(), self.mtg.clone(), self.mte.clone())
         r_a.view(self.q, self.q * t2).copy_(m[:, :self.q * t2])
         return r_a
+
+    def apply_local(self, C, trans):
+        """Q_local^T C (trans) or Q_local C for this shard's block rows
+        C (P*nb x c, device); the local factors of the last factor_local."""
+        plan = self.local_plan
+        cols = C.shape[1] // self.nb
+        ct = plan.pack_cols(C, cols)
+        plan.apply_q(trans, self.tiles, self.tg, self.te, ct, cols)
+        return plan.unpack(ct, cols)
+
+    def apply_merge(self, key, top_a, top_b, trans):
+        """The merge `key`'s Q^T (trans) or Q applied to the stacked R-rows
+        [top_a; top_b] of C (q*nb x c each); returns the two halves."""
+        plan, h = self.merge_plan, self.q * self.nb
+        cols = top_a.shape[1] // self.nb
+        ct = plan.pack_cols(self.torch.cat([top_a, top_b]), cols)
+        tiles, tg, te = self.merge_factors[key]
+        plan.apply_q(trans, tiles, tg, te, ct, cols)
+        out = plan.unpack(ct, cols)
+        return out[:h], out[h:]
 
     def r_matrix(self, rbuf):
         """Upper-triangular n x n R from a q x q tile block."""
@@ -198,12 +287,14 @@ class GpuBackend:
         return R
 
 
-def tall_skinny_qr(A_local, backend, rank, world, dist=None):
+def tall_skinny_qr(A_local, backend, rank, world, dist=None, keep_q=False):
     """Factor the block rows A_local on every rank; rank 0 returns the final
     q x q-tile R block (others return None).  `dist` is torch.distributed
     (send/recv of the R block; NCCL on GPUs, gloo in the CPU tests).
     A_local on the host (page-locked, GpuBackend) streams in while the local
-    factorization runs."""
+    factorization runs.  keep_q keeps every merge's factors on the
+    receiving rank for tall_skinny_apply_q (the local factors stay in the
+    backend until its next factorization)."""
     if getattr(A_local, "is_cuda", True) or not hasattr(backend, "factor_local_host"):
         r = backend.factor_local(A_local)
     else:
@@ -217,8 +308,38 @@ def tall_skinny_qr(A_local, backend, rank, world, dist=None):
                 if recv is None:
                     recv = r.new_empty(r.shape)
                 dist.recv(recv, src=b)
-                r = backend.merge(r, recv)
+                r = backend.merge(r, recv, key=stride) if keep_q else backend.merge(r, recv)
     return r if rank == 0 else None
+
+
+def tall_skinny_apply_q(C_local, backend, rank, world, trans, dist=None):
+    """Q^T C (trans=True) or Q C (trans=False) for the Q of a
+    tall_skinny_qr(..., keep_q=True) on the same ranks: C is block-row
+    sharded like A (C_local: this rank's P*nb rows, on the backend's device).
+    Q = Q_local(r) . merges in round order, so Q^T applies every rank's local
+    reflectors, then each round's merge to the stacked R-rows (the first
+    q*nb rows of each shard) on the receiving rank — the sender's rows go
+    there and come back (point-to-point, like the R exchange); Q applies
+    them in reverse.  Returns this rank's rows of the result."""
+    h = backend.q * backend.nb
+    rounds = merge_rounds(world)
+    c = backend.apply_local(C_local, True) if trans else C_local.clone()
+    for stride, pairs in (rounds if trans else rounds[::-1]):
+        for a, b in pairs:
+            if rank == b:
+                top = c[:h].contiguous()
+                dist.send(top, dst=a)
+                dist.recv(top, src=a)
+                c[:h].copy_(top)
+            elif rank == a:
+                tb = c[:h].new_empty(c[:h].shape)
+                dist.recv(tb, src=b)
+                ta, tb = backend.apply_merge(stride, c[:h], tb, trans)
+                c[:h].copy_(ta)
+                dist.send(tb.contiguous(), dst=b)
+    if not trans:
+        c = backend.apply_local(c, False)
+    return c
 
 
 # ---------------------------------------------------------------------------

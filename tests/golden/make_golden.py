@@ -234,15 +234,26 @@ def main():
     #     merges) through the reference's validate() and
     #     tiled_build(): validity, CP, total weight, trace digest
     def merge_pairs(q, row_a, rows_b):
-        out = []
+        # restated from dist.merge_pairs: per column the two earliest-ready
+        # live rows pair (R_a's row survives, else the lower row); costs
+        # TTQRT 15, TTMQR 2, GEQRT 15; emitted in simulated start order
+        import heapq
+        ev, carry = [], []
         for k in range(1, q + 1):
-            live = [row_a(k)] + [rows_b(i) for i in range(1, k + 1)]
+            live = [(0, k), (0, q + k)] + carry
+            carry = []
+            heapq.heapify(live)
             while len(live) > 1:
-                z = len(live) // 2
-                for t, v in zip(live[len(live) - z:], live[len(live) - 2 * z:len(live) - z]):
-                    out.append(T.ElimEntry(t, v, k))
-                live = live[:len(live) - z]
-        return out
+                t1, r1 = heapq.heappop(live)
+                t2, r2 = heapq.heappop(live)
+                s = max(t1, t2)
+                piv, tgt = (r1, r2) if (r1 == k or (r2 != k and r1 < r2)) else (r2, r1)
+                ev.append((s, tgt, piv, k))
+                heapq.heappush(live, (s + 15, piv))
+                carry.append((s + 32, tgt))
+        ev.sort()
+        row = lambda r: row_a(r) if r <= q else rows_b(r - q)  # noqa: E731
+        return [T.ElimEntry(row(t), row(v), k) for _, t, v, k in ev]
 
     comp = {}
     for p, q, G in ((64, 8, 8), (16, 4, 2), (16, 4, 4), (8192, 8, 1), (8192, 8, 2), (8192, 8, 8)):

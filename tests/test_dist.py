@@ -72,15 +72,50 @@ class CpuOracleBackend:
     def factor_local(self, A_local):
         b = P.build_tree(self.Pp, self.q, "greedy")
         rp = replay_build(A_local.numpy(), b, self.nb)
+        self.local = (rp, *b.trace_arrays()[:2])
+        self.merges = {}
         return self._block(rp.t)
 
-    def merge(self, r_a, r_b):
+    def merge(self, r_a, r_b, key=None):
         rp = Replay.__new__(Replay)
         rp.p, rp.q, rp.nb, rp.ib = 2 * self.q, self.q, self.nb, 32
         rp.t = self._tiles(r_a) + self._tiles(r_b)
         rp.tg, rp.te = {}, {}
         rp.run(self.kinds, self.idx)
+        if key is not None:
+            self.merges[key] = (rp, self.kinds, self.idx)
         return self._block(rp.t[:self.q])
+
+    def apply_local(self, C, trans):
+        return torch.from_numpy(_replay_apply(*self.local, C.numpy(), trans))
+
+    def apply_merge(self, key, top_a, top_b, trans):
+        out = _replay_apply(*self.merges[key], np.vstack([top_a.numpy(), top_b.numpy()]), trans)
+        h = self.q * self.nb
+        return torch.from_numpy(out[:h].copy()), torch.from_numpy(out[h:].copy())
+
+
+def _replay_apply(rp, kinds, idx, C, trans):
+    """LAPACK (dgemqrt / dtpmqrt) application of a replayed factorization's
+    Q^T (trace order, trans='T') or Q (reverse order, 'N') to C."""
+    from scipy.linalg import lapack as L
+    nb, p = rp.nb, rp.p
+    ct = [np.asfortranarray(C[i * nb:(i + 1) * nb]) for i in range(p)]
+    order = range(len(kinds)) if trans else range(len(kinds) - 1, -1, -1)
+    tr = "T" if trans else "N"
+    for t in order:
+        kd = int(kinds[t])
+        a, b, c, _ = (int(x) - 1 for x in idx[t])
+        if kd == 0:  # GEQRT(a, b)
+            ct[a], info = L.dgemqrt(rp.t[a][b], rp.tg[(a, b)], ct[a], side="L", trans=tr)
+        elif kd in (1, 2):  # TTQRT / TSQRT(a, piv=b, k=c)
+            l = nb if kd == 1 else 0
+            v = np.triu(rp.t[a][c]) if l else rp.t[a][c]
+            ct[b], ct[a], info = L.dtpmqrt(l, v, rp.te[(a, c)], ct[b], ct[a], side="L", trans=tr)
+        else:
+            continue
+        assert info == 0
+    return np.vstack(ct)
 
 
 def _full_r(blk, q, nb):
@@ -104,15 +139,32 @@ def _worker(rank, world, port, p, q, nb, out):
     A = _matrix(p, q, nb)
     Pp = p // world
     A_local = torch.from_numpy(A[rank * Pp * nb:(rank + 1) * Pp * nb].copy())
-    r = dist.tall_skinny_qr(A_local, CpuOracleBackend(Pp, q, nb), rank, world, td)
+    be = CpuOracleBackend(Pp, q, nb)
+    r = dist.tall_skinny_qr(A_local, be, rank, world, td, keep_q=True)
+    # distributed apply-Q: Q^T A = [R; 0] on the block rows, Q [I; 0] = Q
+    qta = dist.tall_skinny_apply_q(A_local.clone(), be, rank, world, True, td)
+    E = np.zeros_like(A)
+    E[:q * nb] = np.eye(q * nb)
+    ql = dist.tall_skinny_apply_q(torch.from_numpy(E[rank * Pp * nb:(rank + 1) * Pp * nb].copy()), be, rank, world,
+                                  False, td)
+    parts = [torch.empty_like(ql) for _ in range(world)]
+    td.all_gather(parts, ql)
+    tparts = [torch.empty_like(qta) for _ in range(world)]
+    td.all_gather(tparts, qta)
     if rank == 0:
-        R = row_sign_normalize(_full_r(r, q, nb))
+        Rf = _full_r(r, q, nb)
+        R = row_sign_normalize(Rf)
         Rref = row_sign_normalize(np.linalg.qr(A, mode="r"))
-        out.put(float(np.linalg.norm(R - Rref) / np.linalg.norm(A)))
+        Q = torch.cat(parts).numpy()
+        QtA = torch.cat(tparts).numpy()
+        nA = np.linalg.norm(A)
+        out.put((float(np.linalg.norm(R - Rref) / nA), float(np.linalg.norm(A - Q @ Rf) / nA),
+                 float(np.linalg.norm(Q.T @ Q - np.eye(q * nb))),
+                 float(np.linalg.norm(QtA - np.vstack([Rf, np.zeros((A.shape[0] - q * nb, q * nb))])) / nA)))
     td.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 4])
 def test_gloo_exchange_and_merge(world):
     import torch.multiprocessing as mp
     with socket.socket() as s:
@@ -120,9 +172,10 @@ def test_gloo_exchange_and_merge(world):
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    mp.spawn(_worker, args=(world, port, 8, 2, 64, q), nprocs=world, join=True)
-    err = q.get(timeout=60)
-    assert err <= 1e-13, err
+    mp.spawn(_worker, args=(world, port, 4 * world, 2, 64, q), nprocs=world, join=True)
+    err_r, res, orth, qta = q.get(timeout=60)
+    assert err_r <= 1e-13, err_r
+    assert res <= 1e-14 and orth <= 1e-13 and qta <= 1e-14, (res, orth, qta)
 
 
 @pytest.mark.gpu
@@ -151,3 +204,27 @@ def test_gpu_streamed_local_factorization_matches_device_path():
     r_host = be.factor_local_host(torch.from_numpy(A).pin_memory()).clone()
     torch.cuda.synchronize()
     assert torch.equal(r_dev, r_host)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G,p,q,nb", [(2, 8, 2, 64), (4, 16, 4, 64), (4, 16, 2, 256)])
+def test_gpu_emulated_apply_q(G, p, q, nb):
+    """Distributed apply-Q on the device (shards emulated on one GPU):
+    Q [I; 0] is orthonormal with A = Q R, and Q^T A = [R; 0]."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    A = _matrix(p, q, nb, seed=13)
+    At = torch.from_numpy(A).cuda()
+    bes, r = dist.emulate(At, G, nb, device=torch.device("cuda"), keep=True)
+    Rf = bes[0].r_matrix(r)
+    n = q * nb
+    E = torch.zeros_like(At)
+    E[:n].fill_diagonal_(1.0)
+    Q = torch.cat(dist.emulate_apply_q(bes, E, False))
+    QtA = torch.cat(dist.emulate_apply_q(bes, At, True))
+    nA = torch.linalg.norm(At)
+    assert torch.linalg.norm(At - Q @ Rf) / nA <= 1e-12
+    assert torch.linalg.norm(Q.T @ Q - torch.eye(n, dtype=torch.float64, device="cuda")) <= 1e-12
+    Z = torch.zeros_like(At)
+    Z[:n] = Rf
+    assert torch.linalg.norm(QtA - Z) / nA <= 1e-12

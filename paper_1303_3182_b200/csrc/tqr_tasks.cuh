@@ -236,9 +236,15 @@ __device__ __forceinline__ void tn_acc(double (&acc)[NBK][2], const double* P, i
 // Trailing update of the columns right of panel block b (8 columns per warp,
 // register-resident) — a separate non-inlined function so that its register
 // allocation does not compete with the panel's live state.
+// The chunks holding the next panel block's columns (ch < IB/8) are
+// forwarded into the stacked panel P in shared memory (P is dead during the
+// trailing update) instead of being stored and reloaded: GE keeps only the
+// block's final R rows (< rb0 + IB) for global memory, TT/TS forward every
+// row they hold (the next block's write-back stores them).
 template <int NB, int MODE>
 __device__ __noinline__ void panel_trailing(double* at, double* rt, const double* Vs, const double* Ts, int b, int warp,
-                                            int lane) {
+                                            int lane, double* P) {
+  constexpr int PLD = Smem<NB>::PLD;
   const int rb0 = b * IB;
   const int nch = (NB - rb0 - IB) / 8;
   const int g0 = (MODE == GE) ? rb0 / 8 : 0;
@@ -261,6 +267,19 @@ __device__ __noinline__ void panel_trailing(double* at, double* rt, const double
       load_x<NB>(x, xc, g0, g1, lane);
       warp_apply<NB, true, (MODE == TS ? 2 : MODE)>(x, g0 / (IB / 8), g1 / (IB / 8), Vs, Ts, top, lane, nullptr, b);
     }
+#ifndef TQR_NO_PANEL_FWD
+    if (ch < IB / 8) {
+      const int pc = ch * 8 + (lane >> 2), c2 = 2 * (lane & 3);
+      const int gs = (MODE == GE) ? (rb0 + IB) / 8 : g0;  // first forwarded row group
+      const int poff = (MODE == GE) ? -(rb0 + IB) : IB;    // P row of a tile row
+      if (MODE == GE) store_x<NB>(x, xc, g0, gs, lane);
+#pragma unroll
+      for (int g = 0; g < NB / 8; ++g)
+        if (g >= gs && g < g1)
+          *reinterpret_cast<double2*>(P + poff + 8 * g + c2 + pc * PLD) = make_double2(x[g][0], x[g][1]);
+      continue;
+    }
+#endif
     store_x<NB>(x, xc, g0, g1, lane);
   }
 }
@@ -300,19 +319,27 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
     const int rb0 = b * IB;
     const int nrows = (MODE == GE) ? NB - rb0 : (MODE == TT ? IB + rb0 + IB : IB + NB);
     // ---- load the stacked panel into smem
+#ifndef TQR_NO_PANEL_FWD
+    const bool fwd = b > 0;  // rows forwarded into P by the previous block's trailing update
+#else
+    const bool fwd = false;
+#endif
     if (MODE == GE) {
-      for (int e = tid; e < nrows * IB; e += NT) {
-        const int r = e % nrows, c = e / nrows;
-        P[r + c * PLD] = __ldcg(at + (rb0 + r) + size_t(rb0 + c) * NB);
-      }
+      if (!fwd)
+        for (int e = tid; e < nrows * IB; e += NT) {
+          const int r = e % nrows, c = e / nrows;
+          P[r + c * PLD] = __ldcg(at + (rb0 + r) + size_t(rb0 + c) * NB);
+        }
     } else {
       for (int e = tid; e < IB * IB; e += NT) {
         const int r = e % IB, c = e / IB;
         P[r + c * PLD] = (r <= c) ? __ldcg(rt + (rb0 + r) + size_t(rb0 + c) * NB) : 0.0;
       }
-      const int nb_rows = nrows - IB;
+      // bottom rows: TT forwards rows < rb0, TS all of them
+      const int rf = !fwd ? 0 : (MODE == TT ? rb0 : nrows - IB);
+      const int nb_rows = nrows - IB - rf;
       for (int e = tid; e < nb_rows * IB; e += NT) {
-        const int rr = e % nb_rows, c = e / nb_rows;
+        const int rr = rf + e % nb_rows, c = e / nb_rows;
         double v = 0.0;
         if (MODE == TS || rr <= rb0 + c) v = __ldcg(at + rr + size_t(rb0 + c) * NB);
         P[IB + rr + c * PLD] = v;
@@ -661,7 +688,7 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
     csync();
     mark(3);
     // ---- trailing update of columns rb0+IB .. NB on DMMA, 8 columns per warp
-    panel_trailing<NB, MODE>(at, rt, Vs, Ts, b, warp, lane);
+    panel_trailing<NB, MODE>(at, rt, Vs, Ts, b, warp, lane, P);
     csync();
     mark(4);
   }

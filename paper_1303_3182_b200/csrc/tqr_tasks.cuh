@@ -498,14 +498,27 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
           }
         }
         csync();
-        for (int e = tid; e < 8 * (8 + ncol); e += NT) {
-          const int jr = e / (8 + ncol), cc = e % (8 + ncol);
-          double s = 0.0;
+        // warps 1.. sum W_rest over the warps while warp 0 sums the group
+        // Gram and computes T_g from it (one CTA barrier for both)
+        if (warp > 0) {
+          for (int e = tid - 32; e < 8 * ncol; e += NT - 32) {
+            const int jr = e / ncol, cc = 8 + e % ncol;
+            double s = 0.0;
 #pragma unroll
-          for (int w = 0; w < NW; ++w) s += WP[(w * 8 + jr) * LDW + cc];
-          W[jr * LDW + cc] = s;
+            for (int w = 0; w < NW; ++w) s += WP[(w * 8 + jr) * LDW + cc];
+            W[jr * LDW + cc] = s;
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int jr = (lane >> 3) + 4 * h, cc = lane & 7;
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) s += WP[(w * 8 + jr) * LDW + cc];
+            W[jr * LDW + cc] = s;
+          }
+          __syncwarp();
         }
-        csync();
         // T_g (8x8) = (diag(1/tau) + striu(G_g))^-1 by back substitution;
         // lane cc owns column cc
         if (warp == 0 && lane < 8) {

@@ -160,6 +160,15 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
   // top_s: the block's IB pivot rows of this warp's 8 columns staged in smem
   // (column-major, ld TLD); else read from global
   double w[4][2], ap[4][2];
+#ifndef TQR_W_ONE_CHAIN
+  // V^T X accumulates in two interleaved chains (row halves h of every
+  // 8-row group), summed once: half the dependent-DMMA chain length and a
+  // shorter floating-point accumulation (orthogonality of the applied
+  // transformation)
+  double w2[4][2];
+#pragma unroll
+  for (int nb = KA; nb < KB; ++nb) w2[nb][0] = w2[nb][1] = 0.0;
+#endif
   if (top) {
 #pragma unroll
     for (int nb = KA; nb < KB; ++nb) {
@@ -193,12 +202,23 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int nb = KA; nb < KB; ++nb)
+#ifndef TQR_W_ONE_CHAIN
+            if (!(dg && zero_blk(gg, nb))) dmma(h ? w2[nb] : w[nb], x[rb * 4 + gg][h], bc[h][nb]);
+#else
             if (!(dg && zero_blk(gg, nb))) dmma(w[nb], x[rb * 4 + gg][h], bc[h][nb]);
+#endif
         pf(x, rb * 4 + gg);
       }
     }
     if (rb == NB / IB / 2 - 1) mid(x);  // (a no-op after its first call)
   }
+#ifndef TQR_W_ONE_CHAIN
+#pragma unroll
+  for (int nb = KA; nb < KB; ++nb) {
+    w[nb][0] += w2[nb][0];
+    w[nb][1] += w2[nb][1];
+  }
+#endif
   if (top) {
 #pragma unroll
     for (int nb = KA; nb < KB; ++nb) {

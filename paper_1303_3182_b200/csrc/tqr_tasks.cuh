@@ -587,11 +587,13 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
       for (int pr = warp; pr < 10; pr += NW) {
         const int mb = pr < 4 ? 0 : (pr < 7 ? 1 : (pr < 9 ? 2 : 3));
         const int nbb = pr < 4 ? pr : (pr < 7 ? pr - 3 : (pr < 9 ? pr - 5 : 3));
-        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // two chains (k even/odd steps)
+        // four interleaved chains (k steps mod 4), summed pairwise: T's
+        // consistency with V (orthogonality of the block reflector)
+        double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
         const int r = lane >> 2, c = lane & 3;
-        for (int k = klo; k < khi; k += 8) {
+        for (int k = klo; k < khi; k += 16) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < 4; ++h) {
             const int row = k + 4 * h + c;
             if (k + 4 * h < khi) {
               const double a = vmask_p<NB, MODE>(P[row + (8 * mb + r) * PLD], row, 8 * mb + r);
@@ -600,8 +602,8 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
             }
           }
         }
-        G[(8 * mb + r) + (8 * nbb + 2 * c) * IB] = acc[0][0] + acc[1][0];
-        G[(8 * mb + r) + (8 * nbb + 2 * c + 1) * IB] = acc[0][1] + acc[1][1];
+        G[(8 * mb + r) + (8 * nbb + 2 * c) * IB] = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+        G[(8 * mb + r) + (8 * nbb + 2 * c + 1) * IB] = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
       }
     }
     csync();

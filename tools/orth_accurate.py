@@ -46,8 +46,13 @@ def main():
         A = np.random.default_rng(2).standard_normal((n, n))
         At = torch.from_numpy(A).cuda()
         res = tiled_qr(At, nb=256, algo="greedy")
-        Q, R = res.Q(), res.R()
-        rec = {"ours": {"orth_plain": orth_plain(Q), "orth_comp": orth_compensated(Q),
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        Q = res.Q()
+        e1.record()
+        torch.cuda.synchronize()
+        R = res.R()
+        rec = {"ours": {"form_q_ms": e0.elapsed_time(e1), "orth_plain": orth_plain(Q), "orth_comp": orth_compensated(Q),
                         "resid": (torch.linalg.norm(At - Q @ R) / torch.linalg.norm(At)).item()}}
         del Q, R, res
         torch.cuda.empty_cache()

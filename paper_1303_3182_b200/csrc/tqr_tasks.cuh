@@ -209,6 +209,26 @@ __device__ __forceinline__ unsigned long long ptimer() {
   return tt;
 }
 
+// Global -> shared copy of `total` elements, element e read by ld(e) and
+// written by st(e, v): eight loads per thread are in flight before their
+// stores (a plain loop serializes one global-memory latency per element).
+template <class LD, class ST>
+__device__ __forceinline__ void batched_copy(int total, int tid, LD ld, ST st) {
+  for (int e0 = tid; e0 < total; e0 += 8 * NT) {
+    double v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int e = e0 + t * NT;
+      v[t] = e < total ? ld(e) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int e = e0 + t * NT;
+      if (e < total) st(e, v[t]);
+    }
+  }
+}
+
 template <int NB, int MODE>
 __device__ __forceinline__ double vmask_p(double v, int row, int col) {
   // reflector entry of P row `row`, block column `col`
@@ -324,26 +344,37 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
 #else
     const bool fwd = false;
 #endif
+    // (every shape below has a compile-time row count: GE loads only block
+    // 0, TT's bottom part is always IB rows, TS's is NB rows at block 0)
     if (MODE == GE) {
       if (!fwd)
-        for (int e = tid; e < nrows * IB; e += NT) {
-          const int r = e % nrows, c = e / nrows;
-          P[r + c * PLD] = __ldcg(at + (rb0 + r) + size_t(rb0 + c) * NB);
-        }
+        batched_copy(
+            NB * IB, tid, [&](int e) { return __ldcg(at + e % NB + size_t(e / NB) * NB); },
+            [&](int e, double v) { P[e % NB + (e / NB) * PLD] = v; });
     } else {
-      for (int e = tid; e < IB * IB; e += NT) {
-        const int r = e % IB, c = e / IB;
-        P[r + c * PLD] = (r <= c) ? __ldcg(rt + (rb0 + r) + size_t(rb0 + c) * NB) : 0.0;
-      }
-      // bottom rows: TT forwards rows < rb0, TS all of them
-      const int rf = !fwd ? 0 : (MODE == TT ? rb0 : nrows - IB);
-      const int nb_rows = nrows - IB - rf;
-      for (int e = tid; e < nb_rows * IB; e += NT) {
-        const int rr = rf + e % nb_rows, c = e / nb_rows;
-        double v = 0.0;
-        if (MODE == TS || rr <= rb0 + c) v = __ldcg(at + rr + size_t(rb0 + c) * NB);
-        P[IB + rr + c * PLD] = v;
-      }
+      // pivot triangle and the bottom rows not forwarded by the previous
+      // block (TT: rows rb0 .. rb0+IB-1; TS: all NB rows, block 0 only)
+      constexpr int NBR = (MODE == TT) ? IB : NB;
+      const int rf = (MODE == TT) ? rb0 : 0;
+      const int tot = IB * IB + ((MODE == TT || !fwd) ? NBR * IB : 0);
+      batched_copy(
+          tot, tid,
+          [&](int e) {
+            if (e < IB * IB) {
+              const int r = e % IB, c = e / IB;
+              return (r <= c) ? __ldcg(rt + (rb0 + r) + size_t(rb0 + c) * NB) : 0.0;
+            }
+            const int f = e - IB * IB, rr = rf + f % NBR, c = f / NBR;
+            return (MODE == TS || rr <= rb0 + c) ? __ldcg(at + rr + size_t(rb0 + c) * NB) : 0.0;
+          },
+          [&](int e, double v) {
+            if (e < IB * IB) {
+              P[e % IB + (e / IB) * PLD] = v;
+            } else {
+              const int f = e - IB * IB;
+              P[IB + rf + f % NBR + (f / NBR) * PLD] = v;
+            }
+          });
     }
     csync();
     mark(0);

@@ -710,25 +710,25 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
       tslot[i + size_t(rb0 + j) * IB] = v;
     }
     csync();  // Vs overwrites Tp / G / the scalars
+    // (warp per column, lane per row: row counts are multiples of 32, so
+    // no integer division per element)
     if (MODE == GE) {
-      for (int e = tid; e < nrows * IB; e += NT) {
-        const int r = e % nrows, c = e / nrows;
-        const double v = P[r + c * PLD];
-        at[(rb0 + r) + size_t(rb0 + c) * NB] = v;
-        Vs[swz(rb0 + r, c)] = (r > c) ? v : (r == c ? 1.0 : 0.0);
-      }
+      for (int c = warp; c < IB; c += NW)
+        for (int r = lane; r < nrows; r += 32) {
+          const double v = P[r + c * PLD];
+          at[(rb0 + r) + size_t(rb0 + c) * NB] = v;
+          Vs[swz(rb0 + r, c)] = (r > c) ? v : (r == c ? 1.0 : 0.0);
+        }
     } else {
-      for (int e = tid; e < IB * IB; e += NT) {
-        const int r = e % IB, c = e / IB;
-        if (r <= c) rt[(rb0 + r) + size_t(rb0 + c) * NB] = P[r + c * PLD];
-      }
       const int nb_rows = nrows - IB;
-      for (int e = tid; e < nb_rows * IB; e += NT) {
-        const int rr = e % nb_rows, c = e / nb_rows;
-        const bool live = (MODE == TS) || (rr <= rb0 + c);
-        const double v = live ? P[IB + rr + c * PLD] : 0.0;
-        if (live) at[rr + size_t(rb0 + c) * NB] = v;
-        Vs[swz(rr, c)] = v;
+      for (int c = warp; c < IB; c += NW) {
+        if (lane <= c) rt[(rb0 + lane) + size_t(rb0 + c) * NB] = P[lane + c * PLD];
+        for (int rr = lane; rr < nb_rows; rr += 32) {
+          const bool live = (MODE == TS) || (rr <= rb0 + c);
+          const double v = live ? P[IB + rr + c * PLD] : 0.0;
+          if (live) at[rr + size_t(rb0 + c) * NB] = v;
+          Vs[swz(rr, c)] = v;
+        }
       }
     }
     csync();

@@ -13,5 +13,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 
 timeout 600 python tools/item_trace.py --config c3 --out gpurun_out/item_trace_c3.json > gpurun_out/item_trace_c3.log 2>&1
 timeout 300 python tools/item_trace.py --config c4 --out gpurun_out/item_trace_c4.json > gpurun_out/item_trace_c4.log 2>&1
+[ -n "$WITH_C5_PROBE" ] && timeout 900 python tools/c5_scaling_probe.py > gpurun_out/c5probe.json 2> gpurun_out/c5probe.err
 [ -n "$WITH_NCU_FULL" ] && TAG=ncuF bash tools/gpu_ncu.sh
 echo all done

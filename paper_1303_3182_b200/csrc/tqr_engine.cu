@@ -223,10 +223,12 @@ void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers
   // panel weight: with plenty of update work per SM (C3: ~4700 slab items)
   // a light panel weight lets updates fill the machine (measured best 3.0);
   // with little (C4: ~160) the panels' critical path dominates and a heavy
-  // weight that starts them early is best (measured plateau 8-20)
+  // weight that starts them early is best (measured plateau 8-20; with the
+  // final panels, ~8x an update slab, 8 is best: C4 24.6 vs 25.3 ms at 10,
+  // tools/cost_sweep.sh)
   size_t n_upd = 0;
   for (size_t v = 0; v < n; ++v) n_upd += (items[v].kind >= tqr::UNMQR && items[v].kind <= tqr::TSMQR);
-  const double panel = env_cost("TQR_COST_PANEL", n_upd >= 2000 * size_t(workers) ? 3.0 : 10.0);
+  const double panel = env_cost("TQR_COST_PANEL", n_upd >= 2000 * size_t(workers) ? 3.0 : 8.0);
   for (size_t v = 0; v < n; ++v) w[v] = item_cost(items[v].kind, nb, panel);
   // simulated durations: the panel cost may differ from the one the
   // priorities use (TQR_SIM_PANEL: panel items' duration multiplier)

@@ -380,7 +380,7 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
     mark(0);
     // rows owned by this thread: t and t+NT
     const int r0w = t, r1w = t + NT;
-    const bool own0 = r0w < nrows, own1 = r1w < nrows;
+    const bool own0 = r0w < nrows, own1 = MODE != GE && r1w < nrows;  // GE: nrows <= NT
     auto in_vec = [&](int r, int j) {  // P row r belongs to reflector j's vector part
       if (MODE == GE) return r > j;
       if (MODE == TT) return r >= IB && r <= IB + rb0 + j;
@@ -409,7 +409,7 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
         const double x0 = iv0 ? rv0[jj] : 0.0, x1 = iv1 ? rv1[jj] : 0.0;
         double d[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) d[c] = x0 * rv0[c] + x1 * rv1[c];
+        for (int c = 0; c < 8; ++c) d[c] = (MODE == GE) ? x0 * rv0[c] : fma(x1, rv1[c], x0 * rv0[c]);
         // reduce-scatter 8 values over the warp: lane L ends with value
         // v(L) = 4*bit4 + 2*bit3 + bit2 summed over all 32 lanes
         {
@@ -614,10 +614,11 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
     // ---- block Gram G = V^T V (32x32, upper blocks) on DMMA: warp w takes
     // (m-block, n-block) pairs of the 4x4 block grid with m <= n
     {
-      const int klo = 0, khi = (nrows + 3) & ~3;
+      const int khi = (nrows + 3) & ~3;
       for (int pr = warp; pr < 10; pr += NW) {
         const int mb = pr < 4 ? 0 : (pr < 7 ? 1 : (pr < 9 ? 2 : 3));
         const int nbb = pr < 4 ? pr : (pr < 7 ? pr - 3 : (pr < 9 ? pr - 5 : 3));
+        const int klo = (MODE == GE) ? 8 * nbb : 0;  // GE: V's columns 8nbb.. are zero above row 8nbb
         // four interleaved chains (k steps mod 4), summed pairwise: T's
         // consistency with V (orthogonality of the block reflector)
         double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
@@ -642,8 +643,14 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
     // ---- T_b = U^-1, U = diag(1/tau) + striu(G) (dlarft, forward columnwise):
     // the four 8x8 diagonal blocks by back substitution (lane = column),
     // then two block levels T12 = -T11 G12 T22 with all threads
-    for (int e = tid; e < IB * IB; e += NT) Tp[e] = 0.0;
-    csync();
+    // (warps 4..7 zero the six strictly-lower 8x8 blocks meanwhile; every
+    // upper block is written by the levels below)
+    if (warp >= 4) {
+      for (int e = tid - 128; e < 6 * 64; e += NT - 128) {
+        const int k = e >> 6, bi = k < 1 ? 1 : (k < 3 ? 2 : 3), bj = k < 1 ? 0 : (k < 3 ? k - 1 : k - 3);
+        Tp[(bi * 8 + ((e & 63) >> 3)) * IB + bj * 8 + (e & 7)] = 0.0;
+      }
+    }
     if (warp < 4 && lane < 8) {
       const int g0 = warp * 8, cc = lane;
       double col[8];

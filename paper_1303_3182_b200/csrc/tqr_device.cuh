@@ -71,6 +71,28 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
+// Error-free transformation a + b = s + e (Knuth TwoSum; no reassociation:
+// nvcc does not contract or reorder adds without fast-math).
+__device__ __forceinline__ void two_sum(double& s, double& e, double a, double b) {
+  s = a + b;
+  const double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
+}
+// Compensated DMMA accumulation: the 8x8x4 product is formed from zero (one
+// rounded 4-term sum) and added error-free into hi, the rounding going to lo.
+// The accumulation error then no longer grows with the number of k-steps.
+__device__ __forceinline__ void dmma_comp(double (&hi)[2], double (&lo)[2], double a, double b) {
+  double t[2] = {0.0, 0.0};
+  dmma(t, a, b);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double s, e;
+    two_sum(s, e, hi[h], t[h]);
+    hi[h] = s;
+    lo[h] += e;
+  }
+}
+
 // in-sub-block swizzle: element (a, b) (row, col) of an 8x8 sub-block ->
 // 0..63.  Rows 2k, 2k+1 of a column are adjacent (16-byte staging copies of
 // a column's row pair; one 16-byte load gives the B fragments (2c, r) and
@@ -148,7 +170,11 @@ struct NoMid {
 };
 // One application of reflectors [8*KA, 8*KB) of the block (the 8-column
 // groups KA..KB-1): KA=0, KB=4 is the whole ib-block.
-template <int NB, bool TRANST, int TRI, int RBL, int RBH, int KA, int KB, class PF, class MID>
+// COMP: every accumulation compensated (dmma_comp): used when applying or
+// forming Q (tqr_apply_q), where the rounding of V^T X, T W and V W would
+// otherwise accumulate over the thousands of reflector blocks each entry of
+// Q passes through (orthogonality of the formed Q).
+template <int NB, bool TRANST, int TRI, int RBL, int RBH, int KA, int KB, class PF, class MID, bool COMP = false>
 __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, int rb1, const double* __restrict__ Vs,
                                              const double* __restrict__ Ts, double* top, int lane,
                                              const double* top_s, int drb, PF& pf, MID& mid) {
@@ -160,6 +186,9 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
   // top_s: the block's IB pivot rows of this warp's 8 columns staged in smem
   // (column-major, ld TLD); else read from global
   double w[4][2], ap[4][2];
+  double wl[4][2], wl2[4][2];  // COMP: low parts of the two chains
+#pragma unroll
+  for (int nb = KA; nb < KB; ++nb) wl[nb][0] = wl[nb][1] = wl2[nb][0] = wl2[nb][1] = 0.0;
 #ifndef TQR_W_ONE_CHAIN
   // V^T X accumulates in two interleaved chains (row halves h of every
   // 8-row group), summed once: half the dependent-DMMA chain length and a
@@ -210,6 +239,14 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
           bc[1][nb] = v2.y;
         }
         const bool dg = (TRI != 2) && rb == drb;
+        if constexpr (COMP) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int nb = KA; nb < KB; ++nb)
+              if (!(dg && zero_blk(gg, nb)))
+                dmma_comp(h ? w2[nb] : w[nb], h ? wl2[nb] : wl[nb], x[rb * 4 + gg][h], bc[h][nb]);
+        } else
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -229,6 +266,24 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
     }
     if (rb == NB / IB / 2 - 1) mid(x);  // (a no-op after its first call)
   }
+  if constexpr (COMP) {
+    // W = top + V^T X summed in double-double, rounded once
+#pragma unroll
+    for (int nb = KA; nb < KB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double s, er;
+        two_sum(s, er, w[nb][e], w2[nb][e]);
+        double l = er + (wl[nb][e] + wl2[nb][e]);
+        if (top) {
+          double s2, er2;
+          two_sum(s2, er2, s, ap[nb][e]);
+          s = s2;
+          l += er2;
+        }
+        w[nb][e] = s + l;
+      }
+  } else {
 #ifndef TQR_W_ONE_CHAIN
 #pragma unroll
   for (int nb = KA; nb < KB; ++nb) {
@@ -251,6 +306,7 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
       w[nb][1] += ap[nb][1];
     }
   }
+  }  // !COMP
   // W^T <- W^T T (Q^T) or W^T T^T (Q); T upper triangular
   double tb[2][4][4];
 #pragma unroll
@@ -268,16 +324,28 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
           tb[1][kb][nb] = tp[s3b];
         }
       }
-  double wt[4][2];
+  double wt[4][2], wtl[4][2];
 #pragma unroll
-  for (int nb = KA; nb < KB; ++nb) wt[nb][0] = wt[nb][1] = 0.0;
+  for (int nb = KA; nb < KB; ++nb) wt[nb][0] = wt[nb][1] = wtl[nb][0] = wtl[nb][1] = 0.0;
 #pragma unroll
   for (int kb = KA; kb < KB; ++kb)
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int nb = KA; nb < KB; ++nb)
-        if (TRANST ? (kb <= nb) : (kb >= nb)) dmma(wt[nb], w[kb][h], tb[h][kb][nb]);
+        if (TRANST ? (kb <= nb) : (kb >= nb)) {
+          if constexpr (COMP)
+            dmma_comp(wt[nb], wtl[nb], w[kb][h], tb[h][kb][nb]);
+          else
+            dmma(wt[nb], w[kb][h], tb[h][kb][nb]);
+        }
+  if constexpr (COMP) {
+#pragma unroll
+    for (int nb = KA; nb < KB; ++nb) {
+      wt[nb][0] += wtl[nb][0];
+      wt[nb][1] += wtl[nb][1];
+    }
+  }
   if (top) {
 #pragma unroll
     for (int nb = KA; nb < KB; ++nb) stcg2(top + 8 * nb + 2 * c + r * NB, ap[nb][0] - wt[nb][0], ap[nb][1] - wt[nb][1]);
@@ -293,9 +361,9 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
 #pragma unroll
   for (int rb = 0; rb < NB / IB; ++rb) {
     if (rb >= RBL && rb < RBH && rb >= rb0 && rb < rb1) {
-      double acc3[4][2];
+      double acc3[4][2], acc3l[4][2];
 #pragma unroll
-      for (int gg = 0; gg < 4; ++gg) acc3[gg][0] = acc3[gg][1] = 0.0;
+      for (int gg = 0; gg < 4; ++gg) acc3[gg][0] = acc3[gg][1] = acc3l[gg][0] = acc3l[gg][1] = 0.0;
 #pragma unroll
       for (int kb = KA; kb < KB; ++kb) {
         double bc[2][4];
@@ -310,6 +378,9 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int gg = 0; gg < 4; ++gg)
+            if constexpr (COMP) {
+              if (!(dg && zero_blk(gg, kb))) dmma_comp(acc3[gg], acc3l[gg], wt[kb][h], bc[h][gg]);
+            } else
 #ifdef TQR_DIRECT_ACC
             if (!(dg && zero_blk(gg, kb))) dmma(x[rb * 4 + gg], wt[kb][h], bc[h][gg]);
 #else
@@ -317,6 +388,16 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
 #endif
         pf(x, 32 + rb * 4 + kb);
       }
+      if constexpr (COMP) {
+#pragma unroll
+        for (int gg = 0; gg < 4; ++gg)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            double s, er;
+            two_sum(s, er, x[rb * 4 + gg][e], acc3[gg][e]);
+            x[rb * 4 + gg][e] = s + (er + acc3l[gg][e]);
+          }
+      } else {
 #ifndef TQR_DIRECT_ACC
 #pragma unroll
       for (int gg = 0; gg < 4; ++gg) {
@@ -324,6 +405,7 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
         x[rb * 4 + gg][1] += acc3[gg][1];
       }
 #endif
+      }
     }
   }
   UPROF_MARK_V(12, _tq);
@@ -338,13 +420,13 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
 #define TQR_SPLIT_T 0
 #endif
 template <int NB, bool TRANST, int TRI = 2, int RBL = 0, int RBH = NB / IB, class PF = NoPf, class MID = NoMid,
-          bool SPLIT = (TQR_SPLIT_T != 0)>
+          bool COMP = false, bool SPLIT = (TQR_SPLIT_T != 0)>
 __device__ __forceinline__ void warp_apply(double (&x)[NB / 8][2], int rb0, int rb1, const double* __restrict__ Vs,
                                            const double* __restrict__ Ts, double* top, int lane,
                                            const double* top_s = nullptr, int drb = -1, PF pf = PF(),
                                            MID mid = MID()) {
   if constexpr (!SPLIT) {
-    warp_apply_k<NB, TRANST, TRI, RBL, RBH, 0, 4>(x, rb0, rb1, Vs, Ts, top, lane, top_s, drb, pf, mid);
+    warp_apply_k<NB, TRANST, TRI, RBL, RBH, 0, 4, PF, MID, COMP>(x, rb0, rb1, Vs, Ts, top, lane, top_s, drb, pf, mid);
   } else {
     NoMid none;
     if constexpr (TRANST) {

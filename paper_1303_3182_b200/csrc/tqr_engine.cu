@@ -393,7 +393,7 @@ int num_sms() {
   return sms > 0 ? sms : 148;
 }
 
-cudaError_t run(const DevSched& d, int nb, bool transT, const double* vtiles, double* tiles, double* tg, double* te,
+cudaError_t run(const DevSched& d, int nb, bool apply, bool transT, const double* vtiles, double* tiles, double* tg, double* te,
                 int p, cudaStream_t st, const IoBufs& io = IoBufs{}) {
   cudaError_t e;
   if ((e = cudaMemsetAsync(d.done, 0, size_t(std::max(d.n_items, 1)) * sizeof(int), st)) != cudaSuccess) return e;
@@ -403,14 +403,17 @@ cudaError_t run(const DevSched& d, int nb, bool transT, const double* vtiles, do
   tqrx::g_flags = env_int("TQR_FLAGS", 0);
   tqrx::g_carveout = env_int("TQR_CARVEOUT", -1);
   const int grid = std::min(d.n_items, std::max(1, env_int("TQR_GRID", num_sms())));
+  // factorization: <nb, true, false>; apply-Q: <nb, trans, true> (compensated)
+#define TQR_RUN_NB(NB)                                                                             \
+  case NB:                                                                                         \
+    if (!apply) return launch_exec<NB, true, false>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io); \
+    return transT ? launch_exec<NB, true, true>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io)      \
+                  : launch_exec<NB, false, true>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io);
   switch (nb) {
-    case 64:
-      return transT ? launch_exec<64, true>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io)
-                    : launch_exec<64, false>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io);
-    case 256:
-      return transT ? launch_exec<256, true>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io)
-                    : launch_exec<256, false>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io);
+    TQR_RUN_NB(64)
+    TQR_RUN_NB(256)
   }
+#undef TQR_RUN_NB
   return cudaErrorInvalidValue;
 }
 
@@ -555,7 +558,7 @@ int tqr_factor(tqr_plan* P, double* tiles, double* tg, double* te, void* stream)
     if (!P) throw tqr::ValueError("null plan");
   });
   if (rc) return rc;
-  return cuda_guarded(run(P->fac, P->nb, true, tiles, tiles, tg, te, P->p, static_cast<cudaStream_t>(stream)));
+  return cuda_guarded(run(P->fac, P->nb, false, true, tiles, tiles, tg, te, P->p, static_cast<cudaStream_t>(stream)));
 }
 
 int tqr_factor_io(tqr_plan* P, const double* a_src, int64_t lda, const int* arrive, double* tiles, double* tg,
@@ -567,7 +570,7 @@ int tqr_factor_io(tqr_plan* P, const double* a_src, int64_t lda, const int* arri
   });
   if (rc) return rc;
   IoBufs io{a_src, lda, arrive, r_dst, ldr, r_ready, P->acr, P->anch};
-  return cuda_guarded(run(P->fac, P->nb, true, tiles, tiles, tg, te, P->p, static_cast<cudaStream_t>(stream), io));
+  return cuda_guarded(run(P->fac, P->nb, false, true, tiles, tiles, tg, te, P->p, static_cast<cudaStream_t>(stream), io));
 }
 
 int tqr_plan_arrival_units(const tqr_plan* P, int32_t* n_units, int32_t* units3) {
@@ -617,7 +620,7 @@ int tqr_qr_host(tqr_plan* P, const double* a_host, int64_t lda_h, double* r_host
     if (ck(cudaEventRecord(ev0, st))) break;
     if (ck(cudaStreamWaitEvent(ci, ev0, 0)) || ck(cudaStreamWaitEvent(co, ev0, 0))) break;
     IoBufs io{stage, n, arrive, (P->io & 2) ? r_dev : nullptr, n, (P->io & 2) ? r_ready : nullptr, P->acr, P->anch};
-    if (ck(run(P->fac, nb, true, tiles, tiles, tg, te, P->p, st, io))) break;
+    if (ck(run(P->fac, nb, false, true, tiles, tiles, tg, te, P->p, st, io))) break;
     if (dbg) cudaEventRecord(dk, st);
     bool bad = false;
     // input: one (row chunk x nb columns) block per arrival unit, then raise
@@ -720,7 +723,7 @@ int tqr_apply_q(tqr_plan* P, int trans, const double* tiles, const double* tg, c
   });
   if (rc) return rc;
   const DevSched& d = P->aq[std::make_pair(trans ? 1 : 0, c_cols)];
-  return cuda_guarded(run(d, P->nb, trans != 0, tiles, c_tiles, const_cast<double*>(tg), const_cast<double*>(te),
+  return cuda_guarded(run(d, P->nb, true, trans != 0, tiles, c_tiles, const_cast<double*>(tg), const_cast<double*>(te),
                           P->p, static_cast<cudaStream_t>(stream)));
 }
 

@@ -178,7 +178,8 @@ __device__ __forceinline__ bool is_update_kind(int k) { return k == tqr::UNMQR |
 // finished); the consumers check dependencies on their own barrier and the
 // producer publishes completion flags, so neither waits for the other's
 // memory fences.
-template <int NB, bool TRANST>
+// COMP: apply-Q kernels (update items only, compensated accumulation).
+template <int NB, bool TRANST, bool COMP>
 __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_cur, s_nxt;
@@ -301,35 +302,35 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
     unsigned long long* pprof = P.trace ? P.trace + 4 * size_t(P.n_items) : nullptr;
     switch (I.kind) {
       case tqr::GEQRT:
-        if constexpr (TRANST)
+        if constexpr (TRANST && !COMP)
           panel_item<NB, GE>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), nullptr, P.tg + soff<NB>(P.p, I.i, I.k), tid, pprof);
         break;
       case tqr::TTQRT:
-        if constexpr (TRANST)
+        if constexpr (TRANST && !COMP)
           panel_item<NB, TT>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.k),
                              P.te + soff<NB>(P.p, I.i, I.k), tid, pprof);
         break;
       case tqr::TSQRT:
-        if constexpr (TRANST)
+        if constexpr (TRANST && !COMP)
           panel_item<NB, TS>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.k),
                              P.te + soff<NB>(P.p, I.i, I.k), tid, pprof);
         break;
       case tqr::PACK:
-        if constexpr (TRANST) pack_item<NB>(sm, P, I.i, I.j, tid);
+        if constexpr (TRANST && !COMP) pack_item<NB>(sm, P, I.i, I.j, tid);
         break;
       case tqr::UNPACK:
-        if constexpr (TRANST) unpack_item<NB>(sm, P, I.i, I.j, tid);
+        if constexpr (TRANST && !COMP) unpack_item<NB>(sm, P, I.i, I.j, tid);
         break;
       case tqr::UNMQR:
-        update_consume<NB, GE, TRANST>(sm, P.tiles + toff<NB>(P.p, I.i, I.j), nullptr, I.slab, tid, bars, bars + 2,
+        update_consume<NB, GE, TRANST, COMP>(sm, P.tiles + toff<NB>(P.p, I.i, I.j), nullptr, I.slab, tid, bars, bars + 2,
                                        seq);
         break;
       case tqr::TTMQR:
-        update_consume<NB, TT, TRANST>(sm, P.tiles + toff<NB>(P.p, I.i, I.j), P.tiles + toff<NB>(P.p, I.piv, I.j),
+        update_consume<NB, TT, TRANST, COMP>(sm, P.tiles + toff<NB>(P.p, I.i, I.j), P.tiles + toff<NB>(P.p, I.piv, I.j),
                                        I.slab, tid, bars, bars + 2, seq);
         break;
       case tqr::TSMQR:
-        update_consume<NB, TS, TRANST>(sm, P.tiles + toff<NB>(P.p, I.i, I.j), P.tiles + toff<NB>(P.p, I.piv, I.j),
+        update_consume<NB, TS, TRANST, COMP>(sm, P.tiles + toff<NB>(P.p, I.i, I.j), P.tiles + toff<NB>(P.p, I.piv, I.j),
                                        I.slab, tid, bars, bars + 2, seq);
         break;
     }
@@ -374,26 +375,28 @@ struct DevView {
   int n_items;
 };
 
-template <int NB, bool TRANST>
+template <int NB, bool TRANST, bool COMP>
 cudaError_t launch_exec(const DevView& d, const double* vtiles, double* tiles, double* tg, double* te, int p,
                         unsigned long long* trace, int grid, cudaStream_t st, const IoBufs& io);
 
 // specializations live in tqr_exec_<nb><t|n>.cu
-#define TQR_DECLARE_LAUNCH(NB, TR)                                                                                  \
+#define TQR_DECLARE_LAUNCH(NB, TR, CO)                                                                              \
   template <>                                                                                                      \
-  cudaError_t launch_exec<NB, TR>(const DevView& d, const double* vtiles, double* tiles, double* tg, double* te,  \
+  cudaError_t launch_exec<NB, TR, CO>(const DevView& d, const double* vtiles, double* tiles, double* tg, double* te,  \
                                   int p, unsigned long long* trace, int grid, cudaStream_t st, const IoBufs& io);
-TQR_DECLARE_LAUNCH(64, true)
-TQR_DECLARE_LAUNCH(64, false)
-TQR_DECLARE_LAUNCH(256, true)
-TQR_DECLARE_LAUNCH(256, false)
+TQR_DECLARE_LAUNCH(64, true, false)
+TQR_DECLARE_LAUNCH(64, true, true)
+TQR_DECLARE_LAUNCH(64, false, true)
+TQR_DECLARE_LAUNCH(256, true, false)
+TQR_DECLARE_LAUNCH(256, true, true)
+TQR_DECLARE_LAUNCH(256, false, true)
 
-#define TQR_DEFINE_LAUNCH(NB, TR)                                                                                   \
+#define TQR_DEFINE_LAUNCH(NB, TR, CO)                                                                               \
   template <>                                                                                                      \
-  cudaError_t launch_exec<NB, TR>(const DevView& d, const double* vtiles, double* tiles, double* tg, double* te,  \
+  cudaError_t launch_exec<NB, TR, CO>(const DevView& d, const double* vtiles, double* tiles, double* tg, double* te,  \
                                   int p, unsigned long long* trace, int grid, cudaStream_t st,                     \
                                   const IoBufs& io) {                                                              \
-    auto kern = exec_kernel<NB, TR>;                                                                               \
+    auto kern = exec_kernel<NB, TR, CO>;                                                                               \
     const size_t smem = Smem<NB>::BYTES;                                                                           \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));            \
     if (e != cudaSuccess) return e;                                                                                \

@@ -1,7 +1,7 @@
 // executor instantiation nb=256, Q^T / factor
 #include "tqr_exec.cuh"
 namespace tqrx {
-TQR_DEFINE_LAUNCH(256, true)
+TQR_DEFINE_LAUNCH(256, true, false)
 }
 #ifdef TQR_PROF_UPD
 // instrumented builds only (tools/exec_uprof.py): read and clear the update

@@ -1,0 +1,5 @@
+// executor instantiation nb=64, apply Q^T (compensated)
+#include "tqr_exec.cuh"
+namespace tqrx {
+TQR_DEFINE_LAUNCH(64, true, true)
+}

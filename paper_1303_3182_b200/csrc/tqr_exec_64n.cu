@@ -1,5 +1,5 @@
-// executor instantiation nb=64, Q
+// executor instantiation nb=64, apply Q (compensated)
 #include "tqr_exec.cuh"
 namespace tqrx {
-TQR_DEFINE_LAUNCH(64, false)
+TQR_DEFINE_LAUNCH(64, false, true)
 }

@@ -1,5 +1,5 @@
 // executor instantiation nb=64, Q^T / factor
 #include "tqr_exec.cuh"
 namespace tqrx {
-TQR_DEFINE_LAUNCH(64, true)
+TQR_DEFINE_LAUNCH(64, true, false)
 }

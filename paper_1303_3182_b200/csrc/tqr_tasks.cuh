@@ -98,7 +98,7 @@ __device__ void update_produce(double* sm, const double* __restrict__ vt, const 
 
 // Compute side (8 warps): the warp's 8 columns of the slab stay in
 // registers while all ib-blocks are applied.
-template <int NB, int MODE, bool TRANST>
+template <int NB, int MODE, bool TRANST, bool COMP = false>
 __device__ void update_consume(double* sm, double* xt, double* topt, int slab, int tid, unsigned long long* full,
                                unsigned long long* empty, unsigned seq) {
   using S = Smem<NB>;
@@ -122,7 +122,7 @@ __device__ void update_consume(double* sm, double* xt, double* topt, int slab, i
     const double* Ts = sm + (buf ? S::U_T1 : S::U_T0);
     double* top = (MODE == GE) ? nullptr : topt + size_t(col0) * NB + b * IB;
     const double* top_s = nullptr;  // pivot rows straight from global memory
-    warp_apply<NB, TRANST, MODE, decltype(rbl)::value, decltype(rbh)::value, decltype(pf)>(
+    warp_apply<NB, TRANST, MODE, decltype(rbl)::value, decltype(rbh)::value, decltype(pf), NoMid, COMP>(
         x, r0 / IB, r1 / IB, Vs, Ts, top, lane, top_s, b, pf);
     __syncwarp();
 #ifndef TQR_ABL_NOPROD
@@ -619,9 +619,13 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
         const int mb = pr < 4 ? 0 : (pr < 7 ? 1 : (pr < 9 ? 2 : 3));
         const int nbb = pr < 4 ? pr : (pr < 7 ? pr - 3 : (pr < 9 ? pr - 5 : 3));
         const int klo = (MODE == GE) ? 8 * nbb : 0;  // GE: V's columns 8nbb.. are zero above row 8nbb
-        // four interleaved chains (k steps mod 4), summed pairwise: T's
-        // consistency with V (orthogonality of the block reflector)
+        // T's consistency with the stored V sets the orthogonality of the
+        // block reflector (I - V T V^T orthogonal iff T^-1 + T^-T = V^T V):
+        // the Gram is accumulated compensated (four interleaved chains, each
+        // a double-double hi/lo pair, summed in double-double and rounded
+        // once), so G is V^T V of the stored V to ~1 ulp
         double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+        double accl[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
         const int r = lane >> 2, c = lane & 3;
         for (int k = klo; k < khi; k += 16) {
 #pragma unroll
@@ -630,17 +634,31 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
             if (k + 4 * h < khi) {
               const double a = vmask_p<NB, MODE>(P[row + (8 * mb + r) * PLD], row, 8 * mb + r);
               const double bv = vmask_p<NB, MODE>(P[row + (8 * nbb + r) * PLD], row, 8 * nbb + r);
-              dmma(acc[h], a, bv);
+              dmma_comp(acc[h], accl[h], a, bv);
             }
           }
         }
-        G[(8 * mb + r) + (8 * nbb + 2 * c) * IB] = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
-        G[(8 * mb + r) + (8 * nbb + 2 * c + 1) * IB] = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double hs = acc[0][e], ls = accl[0][e];
+#pragma unroll
+          for (int h = 1; h < 4; ++h) {
+            double t2, er;
+            two_sum(t2, er, hs, acc[h][e]);
+            hs = t2;
+            ls += er + accl[h][e];
+          }
+          G[(8 * mb + r) + (8 * nbb + 2 * c + e) * IB] = hs + ls;
+        }
       }
     }
     csync();
     mark(5);
-    // ---- T_b = U^-1, U = diag(1/tau) + striu(G) (dlarft, forward columnwise):
+    // ---- T_b = U^-1, U = diag(G)/2 + striu(G): dlarft (forward, columnwise)
+    // with each reflector's tau taken as 2 / (v^T v) of its stored v instead
+    // of dlarfg's (beta - alpha) / beta (equal in exact arithmetic; this one
+    // makes every H_j = I - tau v v^T orthogonal to ~1 ulp); tau = 0
+    // (x = 0, H_j = I) is kept:
     // the four 8x8 diagonal blocks by back substitution (lane = column),
     // then two block levels T12 = -T11 G12 T22 with all threads
     // (warps 4..7 zero the six strictly-lower 8x8 blocks meanwhile; every
@@ -653,17 +671,19 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
     }
     if (warp < 4 && lane < 8) {
       const int g0 = warp * 8, cc = lane;
-      double col[8];
+      double col[8], tv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) tv[i] = tau_s[g0 + i] != 0.0 ? 2.0 / G[(g0 + i) * (IB + 1)] : 0.0;
 #pragma unroll
       for (int i = 7; i >= 0; --i) {
         double v = 0.0;
-        if (i == cc) v = tau_s[g0 + i];
+        if (i == cc) v = tv[i];
         if (i < cc) {
           double s = 0.0;
 #pragma unroll
           for (int l = i + 1; l < 8; ++l)
             if (l <= cc) s += G[(g0 + i) + (g0 + l) * IB] * col[l];
-          v = -tau_s[g0 + i] * s;
+          v = -tv[i] * s;
         }
         col[i] = v;
       }

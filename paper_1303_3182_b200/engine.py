@@ -17,7 +17,7 @@ import torch
 
 from . import _lib
 from ._lib import check, lib
-from .qr import EliminationList, QrBuild, build_tree, tiled_build
+from .qr import QrBuild, build_tree, tiled_build
 
 
 def _stream_ptr(stream=None):
@@ -219,8 +219,8 @@ def tiled_qr(A, nb=256, ib=32, algo="greedy", family="TT", bs=None, grasap_i=1, 
     p, q = m // nb, n // nb
     if plan is None:
         if elim is not None:
-            if not isinstance(elim, EliminationList):
-                raise TypeError("elim must be an EliminationList")
+            if not (hasattr(elim, "p") and hasattr(elim, "q") and hasattr(elim, "__iter__")):
+                raise TypeError("elim must be an elimination list (.p .q and entries .i .piv .k)")
             if (elim.p, elim.q) != (p, q):
                 raise ValueError(f"list is for {elim.p}x{elim.q} tiles, matrix has {p}x{q}")
             build = tiled_build(elim, family)

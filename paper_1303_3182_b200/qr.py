@@ -36,11 +36,33 @@ class ElimEntry:
 
 
 def _to_array(entries):
-    n = len(entries)
-    a = np.empty((n, 4), dtype=np.int32)
-    if n:
-        a[:] = [(e.i, e.piv, e.k, e.step) for e in entries]
+    """(n, 4) int32 (i, piv, k, step) of any iterable of entries exposing
+    .i .piv .k (and optionally .step) — this package's ElimEntry or the
+    reference's (qr.py:31-38)."""
+    rows = [(e.i, e.piv, e.k, getattr(e, "step", 0)) for e in entries]
+    a = np.empty((len(rows), 4), dtype=np.int32)
+    if rows:
+        a[:] = rows
     return a
+
+
+def elim_array(elim):
+    """(n, 4) int32 array of any elimination list: this package's
+    EliminationList or one duck-typed like the reference's (``.p .q`` plus
+    iteration over entries, qr.py:41-55)."""
+    return _to_array(list(elim))
+
+
+def _validate_any(elim):
+    """EliminationList.validate() semantics (qr.py:56-83) for any list-like
+    object, run by the C++ validator (same messages)."""
+    a = elim_array(elim)
+    msg = C.create_string_buffer(512)
+    rc = lib().tqr_elim_validate(int(elim.p), int(elim.q), ptr_i32(a), len(a), msg, 512)
+    if rc == 1:
+        raise ValueError(msg.value.decode())
+    check(rc)
+    return True
 
 
 def _from_array(a):
@@ -66,13 +88,7 @@ class EliminationList:
         return _to_array(self.entries)
 
     def validate(self):
-        a = self.array()
-        msg = C.create_string_buffer(512)
-        rc = lib().tqr_elim_validate(self.p, self.q, ptr_i32(a), len(a), msg, 512)
-        if rc == 1:
-            raise ValueError(msg.value.decode())
-        check(rc)
-        return True
+        return _validate_any(self)
 
     def normalized(self):
         a = self.array()
@@ -329,24 +345,40 @@ class QrBuild:
         return [(u, v, cause[c]) for u, v, c in e[:n.value].tolist()]
 
     def run_list(self, elim: EliminationList):
-        a = elim.array()
+        """Tiled translation of ``elim`` (qr.py:520-532): this package's
+        EliminationList or the reference's (entries read as .i .piv .k)."""
+        a = elim_array(elim)
         h = C.c_void_p()
-        w = np.asarray(self.weights.qr_vector(), dtype=np.int64)
+        w = _weights_arg(self.weights)
         check(lib().tqr_tiled_build(self.p, self.q, ptr_i32(a), len(a), int(self.family == "TS"), ptr_i64(w),
                                     int(self.keep_trace), int(self.record_updates), 0, C.byref(h)))
         return self._adopt(h, elim)
 
 
 def _weights_arg(weights):
-    w = (weights if weights is not None else WeightModel.qr_tt()).qr_vector()
+    """Per-kind weight vector (C-ABI kind order, -1 where the model has no
+    weight) of this package's WeightModel or any model answering
+    ``weights[kind]`` / raising KeyError like the reference's
+    (taskgraph.py:139-146)."""
+    if weights is None:
+        weights = WeightModel.qr_tt()
+    if hasattr(weights, "qr_vector"):
+        return np.asarray(weights.qr_vector(), dtype=np.int64)
+    w = []
+    for k in QR_KINDS:
+        try:
+            w.append(int(weights[k]))
+        except KeyError:
+            w.append(-1)
     return np.asarray(w, dtype=np.int64)
 
 
 def tiled_build(elim: EliminationList, family="TT", weights=None, keep_trace=True,
                 record_updates=False, validate=True) -> QrBuild:
-    """Tiled translation of any valid elimination list (qr.py:535-540)."""
+    """Tiled translation of any valid elimination list (qr.py:535-540); the
+    list may be the reference's own EliminationList (duck-typed)."""
     if validate:
-        elim.validate()
+        _validate_any(elim)
     b = QrBuild(elim.p, elim.q, family, weights, keep_trace, record_updates)
     return b.run_list(elim)
 

@@ -4,9 +4,9 @@ Mirrors the pieces of the reference's core engine that the QR path uses
 (pkg/src/tiledag/taskgraph.py): the kernel tags (:19-40), TileRef (:48-54),
 Task (:57-75), WeightModel (:78-146) and the hazard DAG of a QR trace
 (build_from_trace, :262-322) with Backflow/earliest times (annotate_cp,
-:338-362).  The hazard edges of a QrBuild trace are computed by the C++
-schedule compiler (the same edges drive the device dependency counters);
-generic traces fall back to a Python statement of the same rule.
+:338-362).  Hazard edges always come from the C++ schedule compiler (the
+same edges drive the device dependency counters), for this package's traces
+and for the reference's own Task lists alike.
 """
 from __future__ import annotations
 
@@ -180,37 +180,55 @@ class TaskGraph:
         return [t.id for t in self.tasks]  # trace-built: edges go forward
 
 
-def _python_hazards(trace):
-    edges, last_write, readers = [], {}, {}
-    for t in trace:
-        for tile in t.reads:
-            w = last_write.get(tile)
-            if w is not None:
-                edges.append((w, t.id, RAW))
-            readers.setdefault(tile, []).append(t.id)
-        for tile in t.writes:
-            rs = readers.get(tile)
-            if rs:
-                edges.extend((r, t.id, WAR) for r in rs if r != t.id)
-            elif tile in last_write:
-                edges.append((last_write[tile], t.id, WAW))
-            last_write[tile] = t.id
-            readers[tile] = []
-    seen, uniq = set(), []
-    for e in edges:
-        if (e[0], e[1]) not in seen:
-            seen.add((e[0], e[1]))
-            uniq.append(e)
-    return uniq
+def _trace_edges(trace):
+    """Hazard edges of any QR trace (this package's or the reference's Task
+    objects: .id .kind .indices), computed by the C++ compiler
+    (tqr_trace_build + tqr_build_hazard_edges, the rule of
+    taskgraph.py:262-322)."""
+    import ctypes as C
+
+    import numpy as np
+
+    from . import _lib
+
+    tasks = list(trace)
+    n = len(tasks)
+    kind = np.empty(max(n, 1), dtype=np.int8)
+    idx = np.full((max(n, 1), 4), -1, dtype=np.int32)
+    code = {k: c for c, k in enumerate(QR_KINDS)}
+    p = q = 1
+    for t, task in enumerate(tasks):
+        if task.kind not in code:
+            raise ValueError(f"build_from_trace: {task.kind} is not a QR kernel")
+        kind[t] = code[task.kind]
+        ind = tuple(task.indices)
+        idx[t, :len(ind)] = ind
+        rows = ind[:1] if task.kind in (GEQRT, UNMQR) else ind[:2]
+        p = max(p, *rows)
+        q = max(q, ind[-1])
+    h = C.c_void_p()
+    L = _lib.lib()
+    _lib.check(L.tqr_trace_build(p, q, kind.ctypes.data_as(_lib.i8p), _lib.ptr_i32(idx), n, C.byref(h)))
+    try:
+        cnt = C.c_int64()
+        _lib.check(L.tqr_build_hazard_edges(h, None, 0, C.byref(cnt)))
+        e = np.empty((max(cnt.value, 1), 3), dtype=np.int32)
+        _lib.check(L.tqr_build_hazard_edges(h, _lib.ptr_i32(e), cnt.value, C.byref(cnt)))
+    finally:
+        L.tqr_build_free(h)
+    ids = [t.id for t in tasks]
+    cause = (RAW, WAR, WAW)
+    return [(ids[u], ids[v], cause[c]) for u, v, c in e[:cnt.value].tolist()]
 
 
 def build_from_trace(trace) -> TaskGraph:
-    """Hazard DAG of a QR trace (taskgraph.py:262-322); traces produced by a
-    QrBuild use the C++ compiler's edges, the ones the device runs on."""
+    """Hazard DAG of a QR trace (taskgraph.py:262-322): a QrBuild's trace uses
+    its compiled edges (the ones the device runs on), any other QR trace —
+    e.g. the reference's own Task list — goes through the same C++ rule."""
     build = getattr(trace, "build", None)
     if build is not None:
         return TaskGraph(trace, build.hazard_edges())
-    return TaskGraph(trace, _python_hazards(trace))
+    return TaskGraph(trace, _trace_edges(trace))
 
 
 def annotate_cp(graph: TaskGraph, weights: WeightModel) -> CpAnnotation:

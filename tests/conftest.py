@@ -21,3 +21,19 @@ def pytest_configure(config):
 def golden():
     with gzip.open(os.path.join(GOLDEN, "schedules.json.gz"), "rt") as fh:
         return json.load(fh)
+
+
+def reference_tiledag():
+    """The reference package itself (test infrastructure only): the pip-
+    installed copy under baseline/_ref (travels to the GPU box) or the
+    read-only source tree in this container; None when neither exists."""
+    import importlib
+    for path in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(path, "tiledag")):
+            if path not in sys.path:
+                sys.path.append(path)
+            try:
+                return importlib.import_module("tiledag")
+            except ImportError:
+                return None
+    return None

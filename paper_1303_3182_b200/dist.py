@@ -20,10 +20,6 @@ device work so the control flow is testable with gloo on CPU.
 from __future__ import annotations
 
 import ctypes as C
-import json
-import os
-import statistics
-import time
 
 import numpy as np
 
@@ -340,124 +336,3 @@ def tall_skinny_apply_q(C_local, backend, rank, world, trans, dist=None):
     if not trans:
         c = backend.apply_local(c, False)
     return c
-
-
-# ---------------------------------------------------------------------------
-# benchmark (bench.py --gpus N, or --config c5 on one GPU)
-
-def bench_main(args, cfg, make_matrix, Clocks, cpu_replay_rate):
-    import torch
-    import torch.distributed as td
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        td.init_process_group("nccl", device_id=dev)
-    nb, m, n = cfg["nb"], cfg["m"], cfg["n"]
-    p, q = m // nb, n // nb
-    if p % world:
-        raise SystemExit(f"p={p} not divisible by world={world}")
-    P = p // world
-    rows = P * nb
-    A_host = make_matrix(cfg, rows=rows, row0=rank * rows)
-    A = torch.from_numpy(A_host).to(dev)
-    be = GpuBackend(P, q, nb, dev)
-    flops = 2.0 * n * n * (m - n / 3.0)
-
-    def step():
-        return tall_skinny_qr(A, be, rank, world, td if world > 1 else None)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        td.barrier()
-    clk = Clocks(local).start() if rank == 0 else None
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    start.record()
-    for _ in range(args.steps):
-        out = step()
-    end.record()
-    torch.cuda.synchronize()
-    if world > 1:
-        td.barrier()
-    ms = start.elapsed_time(end) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        td.all_reduce(t, op=td.ReduceOp.MAX)
-    ms = float(t.item())
-    clocks = clk.stop() if clk else None
-    # e2e through the public API: each rank's shard H2D from (registered,
-    # page-locked) host memory, the factorization, R back to the host
-    e2e = None
-    if not getattr(args, "no_e2e", False):
-        import ctypes as C
-        cudart = torch.cuda.cudart()
-        host = torch.from_numpy(A_host)
-        reg = int(cudart.cudaHostRegister(host.data_ptr(), host.numel() * 8, 0)) == 0
-        R_host = torch.empty((n, n), dtype=torch.float64).pin_memory()
-        ne = max(1, min(args.steps, 2))
-
-        def e2e_step():
-            out = tall_skinny_qr(host if reg else host.to(dev), be, rank, world, td if world > 1 else None)
-            if rank == 0:
-                R_host.copy_(be.r_matrix(out), non_blocking=True)
-
-        e2e_step()
-        torch.cuda.synchronize()
-        if world > 1:
-            td.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(ne):
-            e2e_step()
-        e1.record()
-        torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1) / ne], dtype=torch.float64, device=dev)
-        if world > 1:
-            td.all_reduce(te, op=td.ReduceOp.MAX)
-        if reg:
-            cudart.cudaHostUnregister(host.data_ptr())
-        e_ms = float(te.item())
-        e2e = {"value": round(flops / (e_ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s", "ms_per_step": round(e_ms, 3),
-               "api": "dist.tall_skinny_qr (page-locked host shard streamed in, R to host on rank 0)",
-               "h2d_bytes_per_step": int(m) * int(n) * 8, "d2h_bytes_per_step": int(n) * int(n) * 8,
-               "host_registered": reg}
-    peak = None
-    if rank == 0:
-        import ctypes as C
-        from . import _lib
-        pk = C.c_double()
-        _lib.check(_lib.lib().tqr_fp64_peak(C.byref(pk), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
-        peak = pk.value * world
-    if rank == 0:
-        R = be.r_matrix(out)
-        ok = bool(torch.isfinite(R).all().item())
-        cpu = None
-        if not args.no_cpu_baseline and world == 1:
-            sub = dict(cfg, m=min(m, 1024 * nb))
-            rate, desc, thr = cpu_replay_rate(sub, A_host[:sub["m"]])
-            cpu = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": thr, "kind": "port", "sample": desc}
-        print(json.dumps({
-            "metric": "tiled QR fp64 GFLOP/s (2n^2(m-n/3))", "value": round(flops / (ms * 1e-3) / 1e9, 2),
-            "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "c5", "m": m, "n": n, "nb": nb, "ib": 32, "tree": "greedy local + binary TT merge",
-                       "seed": cfg["seed"], "dist": "uniform(-1,1), row chunk c from default_rng([seed, c])",
-                       "parallelism": f"block rows over {world} GPU(s), NCCL p2p R merges",
-                       "l2": "inputs > 126 MB L2 (no flush needed)"},
-            "gpu_launches": (2 + 3 * (world - 1)) * args.steps,
-            "roofline": {"bound": "tensor", "achieved": round(flops / (ms * 1e-3) / 1e12, 3), "peak": round(peak, 3),
-                         "unit": "TFLOP/s", "frac": round(flops / (ms * 1e-3) / 1e12 / peak, 4), "traffic": None,
-                         "kernel": "exec_kernel (local factorization + merges)",
-                         "peak_source": "live DMMA.8x8x4 probe x n_gpus"},
-            "clocks": clocks, "cpu_baseline": cpu, "e2e": e2e,
-            "check": {"r_finite": ok},
-        }))
-    if world > 1:
-        td.destroy_process_group()

@@ -24,6 +24,9 @@ M, N, NB = 2097152, 2048, 256
 def _need_gpu():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
     free, total = torch.cuda.mem_get_info()
     if free < 150e9:
         pytest.skip(f"needs ~150 GB of free device memory ({free / 1e9:.0f} GB free)")

@@ -14,7 +14,8 @@
  * Every function returns 0 on success or a negative TQR_E* status; the
  * message is available from tqr_last_error() (thread-local).  Device
  * pointers are plain CUDA device addresses owned by the caller; `stream` is
- * a cudaStream_t passed as void*.  Plans are immutable after creation.
+ * a cudaStream_t passed as void*.  Plans are immutable after creation and
+ * may be launched concurrently on several streams (per-launch scratch slots).
  */
 #ifndef TQR_H
 #define TQR_H
@@ -138,7 +139,7 @@ int tqr_factor_io(tqr_plan* plan, const double* a_src, int64_t lda, const int* a
  * pinned row-major R (ldr_h) out, every transfer overlapped with the
  * factorization.  With io = 1 only A streams in (r_host, r_dev, r_ready may
  * be NULL; the factored tiles stay in `tiles`).  Enqueues on `stream` the executor, on `copy_in` the
- * nb-column blocks of A (one 2D copy each, in tqr_plan_arrival_order) each
+ * nb-column blocks of A (one 2D copy each, in tqr_plan_arrival_units order) each
  * followed by its arrival flag, and on `copy_out` one wait + copy per tile
  * row of R; returns at once, `stream` completes after all three.  Device
  * scratch: stage (m*n doubles), arrive (q ints), r_dev (n*n doubles),

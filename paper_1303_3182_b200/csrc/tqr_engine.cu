@@ -16,6 +16,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <numeric>
 #include <queue>
 #include <string>
@@ -102,22 +104,44 @@ __global__ void __launch_bounds__(256) peak_kernel(double* out, int iters) {
 // ---------------------------------------------------------------------------
 // host: schedule compilation
 
+// Per-launch scratch of a schedule: the items' done flags and the dequeue
+// counter.  A plan may be launched concurrently on several streams (the
+// plan itself is immutable): each launch takes the next of kSlots slots
+// round-robin and, on its own stream, first waits for the launch that used
+// the slot before, so two in-flight launches never share flags.
+constexpr int kSlots = 2;
+struct ScratchSlot {
+  int* done = nullptr;
+  int* queue = nullptr;
+  cudaEvent_t ev = nullptr;
+  bool used = false;
+};
+struct ScratchPool {
+  std::mutex mu;
+  ScratchSlot slots[kSlots];
+  int n_alloc = 0;
+  unsigned next = 0;
+  ~ScratchPool() {
+    for (int i = 0; i < n_alloc; ++i) {
+      cudaFree(slots[i].done);
+      cudaFree(slots[i].queue);
+      if (slots[i].ev) cudaEventDestroy(slots[i].ev);
+    }
+  }
+};
+
 struct DevSched {
   Item* items = nullptr;
   int32_t* preds = nullptr;
-  int* done = nullptr;
-  int* queue = nullptr;
   int n_items = 0;
   int64_t n_preds = 0;
+  std::shared_ptr<ScratchPool> scratch = std::make_shared<ScratchPool>();
   void free_all() {
     cudaFree(items);
     cudaFree(preds);
-    cudaFree(done);
-    cudaFree(queue);
     items = nullptr;
     preds = nullptr;
-    done = nullptr;
-    queue = nullptr;
+    scratch.reset();
   }
 };
 
@@ -321,8 +345,6 @@ void upload(DevSched& d, const std::vector<Item>& items, const std::vector<int32
   };
   ck(cudaMalloc(&d.items, std::max<size_t>(1, items.size()) * sizeof(Item)));
   ck(cudaMalloc(&d.preds, std::max<size_t>(1, preds.size()) * sizeof(int32_t)));
-  ck(cudaMalloc(&d.done, std::max<size_t>(1, items.size()) * sizeof(int)));
-  ck(cudaMalloc(&d.queue, sizeof(int)));
   ck(cudaMemcpy(d.items, items.data(), items.size() * sizeof(Item), cudaMemcpyHostToDevice));
   if (!preds.empty()) ck(cudaMemcpy(d.preds, preds.data(), preds.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
 }
@@ -341,6 +363,7 @@ struct tqr_plan {
   int acr = 1, anch = 1;
   DevSched fac;
   std::map<std::pair<int, int>, DevSched> aq;  // (trans, c_cols) -> apply-Q schedule
+  std::mutex aq_mu;                             // guards aq (concurrent tqr_apply_q callers)
   ~tqr_plan() {
     fac.free_all();
     for (auto& kv : aq) kv.second.free_all();
@@ -396,10 +419,27 @@ int num_sms() {
 cudaError_t run(const DevSched& d, int nb, bool apply, bool transT, const double* vtiles, double* tiles, double* tg, double* te,
                 int p, cudaStream_t st, const IoBufs& io = IoBufs{}) {
   cudaError_t e;
-  if ((e = cudaMemsetAsync(d.done, 0, size_t(std::max(d.n_items, 1)) * sizeof(int), st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(d.queue, 0, sizeof(int), st)) != cudaSuccess) return e;
   if (d.n_items == 0) return cudaSuccess;
-  DevView v{d.items, d.preds, d.done, d.queue, d.n_items};
+  ScratchSlot* sl = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(d.scratch->mu);
+    ScratchPool& pool = *d.scratch;
+    const int k = int(pool.next++ % unsigned(kSlots));
+    if (k >= pool.n_alloc) {
+      ScratchSlot& ns = pool.slots[pool.n_alloc];
+      if ((e = cudaMalloc(&ns.done, size_t(d.n_items) * sizeof(int))) != cudaSuccess) return e;
+      if ((e = cudaMalloc(&ns.queue, sizeof(int))) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&ns.ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+      sl = &ns;
+      ++pool.n_alloc;
+    } else {
+      sl = &pool.slots[k];
+    }
+    if (sl->used && (e = cudaStreamWaitEvent(st, sl->ev, 0)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(sl->done, 0, size_t(d.n_items) * sizeof(int), st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(sl->queue, 0, sizeof(int), st)) != cudaSuccess) return e;
+  }
+  DevView v{d.items, d.preds, sl->done, sl->queue, d.n_items};
   tqrx::g_flags = env_int("TQR_FLAGS", 0);
   tqrx::g_carveout = env_int("TQR_CARVEOUT", -1);
   const int grid = std::min(d.n_items, std::max(1, env_int("TQR_GRID", num_sms())));
@@ -409,12 +449,19 @@ cudaError_t run(const DevSched& d, int nb, bool apply, bool transT, const double
     if (!apply) return launch_exec<NB, true, false>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io); \
     return transT ? launch_exec<NB, true, true>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io)      \
                   : launch_exec<NB, false, true>(v, vtiles, tiles, tg, te, p, g_trace, grid, st, io);
-  switch (nb) {
-    TQR_RUN_NB(64)
-    TQR_RUN_NB(256)
-  }
+  auto launch = [&]() -> cudaError_t {
+    switch (nb) {
+      TQR_RUN_NB(64)
+      TQR_RUN_NB(256)
+    }
+    return cudaErrorInvalidValue;
+  };
 #undef TQR_RUN_NB
-  return cudaErrorInvalidValue;
+  e = launch();
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(d.scratch->mu);
+  sl->used = true;
+  return cudaEventRecord(sl->ev, st);
 }
 
 int cuda_guarded(cudaError_t e) {
@@ -590,6 +637,9 @@ int tqr_qr_host(tqr_plan* P, const double* a_host, int64_t lda_h, double* r_host
     if (!(P->io & 1)) throw tqr::ValueError("tqr_qr_host needs a plan made with io & 1 (streamed input)");
     if (!a_host || !stage || !arrive) throw tqr::ValueError("null buffer");
     if ((P->io & 2) && (!r_host || !r_dev || !r_ready)) throw tqr::ValueError("null R buffer");
+    const int64_t nn = int64_t(P->q) * P->nb;
+    if (lda_h < nn) throw tqr::ValueError("lda_h must be >= n (row-major A, unit column stride)");
+    if ((P->io & 2) && ldr_h < nn) throw tqr::ValueError("ldr_h must be >= n (row-major R, unit column stride)");
     if (!stream_memops()) throw std::runtime_error("CUDA stream memory operations unavailable");
   });
   if (rc) return rc;
@@ -614,6 +664,7 @@ int tqr_qr_host(tqr_plan* P, const double* a_host, int64_t lda_h, double* r_host
     cudaEventCreate(&dout);
     cudaEventRecord(d0, st);
   }
+  bool launched = false;
   do {
     if (ck(cudaMemsetAsync(arrive, 0, P->arrival.size() / 3 * sizeof(int), st))) break;
     if ((P->io & 2) && ck(cudaMemsetAsync(r_ready, 0, size_t(q) * sizeof(int), st))) break;
@@ -621,6 +672,7 @@ int tqr_qr_host(tqr_plan* P, const double* a_host, int64_t lda_h, double* r_host
     if (ck(cudaStreamWaitEvent(ci, ev0, 0)) || ck(cudaStreamWaitEvent(co, ev0, 0))) break;
     IoBufs io{stage, n, arrive, (P->io & 2) ? r_dev : nullptr, n, (P->io & 2) ? r_ready : nullptr, P->acr, P->anch};
     if (ck(run(P->fac, nb, false, true, tiles, tiles, tg, te, P->p, st, io))) break;
+    launched = true;
     if (dbg) cudaEventRecord(dk, st);
     bool bad = false;
     // input: one (row chunk x nb columns) block per arrival unit, then raise
@@ -650,6 +702,18 @@ int tqr_qr_host(tqr_plan* P, const double* a_host, int64_t lda_h, double* r_host
     if (ck(cudaEventRecord(ev1, ci)) || ck(cudaEventRecord(ev2, co))) break;
     if (ck(cudaStreamWaitEvent(st, ev1, 0)) || ck(cudaStreamWaitEvent(st, ev2, 0))) break;
   } while (false);
+  if (e != cudaSuccess && launched) {
+    // the executor is running and its PACK items spin on arrival flags a
+    // failed copy will never raise: release it (every flag nonzero) on a
+    // fresh stream so the kernel drains (its output is garbage; the error
+    // is returned) instead of hanging the device
+    cudaStream_t rs = nullptr;
+    if (cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking) == cudaSuccess) {
+      cudaMemsetAsync(arrive, 0x01, P->arrival.size() / 3 * sizeof(int), rs);
+      cudaStreamSynchronize(rs);
+      cudaStreamDestroy(rs);
+    }
+  }
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   cudaEventDestroy(ev2);
@@ -674,6 +738,7 @@ int tqr_apply_q(tqr_plan* P, int trans, const double* tiles, const double* tg, c
     if (!P) throw tqr::ValueError("null plan");
     if (c_cols < 1) throw tqr::ValueError("c_cols must be >= 1");
     auto key = std::make_pair(trans ? 1 : 0, c_cols);
+    std::lock_guard<std::mutex> lk(P->aq_mu);
     if (P->aq.count(key)) return;
     // reflector replay: forward trace order for Q^T, reverse for Q
     // (oracle recipe: SURVEY.md App. B.1 step 4); updates skipped.
@@ -722,7 +787,11 @@ int tqr_apply_q(tqr_plan* P, int trans, const double* tiles, const double* tg, c
     P->aq[key] = d;
   });
   if (rc) return rc;
-  const DevSched& d = P->aq[std::make_pair(trans ? 1 : 0, c_cols)];
+  DevSched d;
+  {
+    std::lock_guard<std::mutex> lk(P->aq_mu);
+    d = P->aq[std::make_pair(trans ? 1 : 0, c_cols)];
+  }
   return cuda_guarded(run(d, P->nb, true, trans != 0, tiles, c_tiles, const_cast<double*>(tg), const_cast<double*>(te),
                           P->p, static_cast<cudaStream_t>(stream)));
 }

@@ -90,8 +90,13 @@ class Plan:
         as soon as it is complete (zeros strictly below the diagonal tiles
         must already be there).  Returns when R_host is filled."""
         assert self.io == (self.IO_IN | self.IO_OUT)
-        assert A_host.is_pinned() and R_host.is_pinned()
-        assert A_host.shape == (self.m, self.n) and R_host.shape == (self.n, self.n)
+        if not (A_host.is_pinned() and R_host.is_pinned()):
+            raise ValueError("A_host and R_host must be page-locked (pin_memory())")
+        if A_host.shape != (self.m, self.n) or R_host.shape != (self.n, self.n):
+            raise ValueError(f"need A_host {self.m}x{self.n} and R_host {self.n}x{self.n}")
+        for name, t in (("A_host", A_host), ("R_host", R_host)):
+            if t.dtype != torch.float64 or t.stride(1) != 1 or t.stride(0) < t.shape[1]:
+                raise ValueError(f"{name} must be fp64 row-major with unit column stride")
         cs = torch.cuda.current_stream()
         check(lib().tqr_qr_host(self._h, C.c_void_p(A_host.data_ptr()), A_host.stride(0),
                                 C.c_void_p(R_host.data_ptr()), R_host.stride(0), _vp(bufs.stage), _vp(bufs.arrive),
@@ -190,7 +195,8 @@ def tiled_qr_host(A_host, R_host=None, nb=256, algo="greedy", family="TT", bs=No
     factorization (PACK/UNPACK work items, tqr_qr_host).  A_host: fp64
     m x n row-major (pinned for full overlap); returns (R_host, TiledQR)."""
     A_host = torch.as_tensor(A_host, dtype=torch.float64)
-    A_host = A_host if A_host.is_pinned() else A_host.contiguous().pin_memory()
+    if not (A_host.is_pinned() and A_host.stride(1) == 1 and A_host.stride(0) >= A_host.shape[1]):
+        A_host = A_host.contiguous().pin_memory()  # row-major, unit column stride
     m, n = A_host.shape
     if plan is None:
         build = build_tree(m // nb, n // nb, algo, family=family, bs=bs, grasap_i=grasap_i)

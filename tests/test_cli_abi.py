@@ -62,3 +62,24 @@ def test_error_status_mapping():
     assert rc == _lib.TQR_EVALUE and lib.tqr_last_error() == b"need p >= q >= 1"
     with pytest.raises(ValueError, match="unknown coarse algorithm 'bogus'"):
         _lib.check(lib.tqr_coarse_schedule(4, 3, b"bogus", None, None, 0, C.byref(n), C.byref(x)))
+
+
+@pytest.mark.parametrize("cmd,kind,key", [("qr-coarse --p 15 --q 6 --algo fibonacci --check", "coarse", "fibonacci"),
+                                          ("qr-tiled --p 15 --q 6 --algo plasmatree --bs 5 --check", "tiled",
+                                           "plasmatree/5"),
+                                          ("qr-tiled --p 15 --q 6 --algo binarytree --check", "tiled",
+                                           "binarytree")])
+def test_cli_check_compares_every_cell(monkeypatch, capsys, cmd, kind, key):
+    """--check compares all 15x6 cells (reference cli.py:119-127, :141-148):
+    every table passes as built, and a corrupted cell in an inner row is
+    reported by its (i,k) with exit code 1."""
+    from paper_1303_3182_b200 import cli
+    assert main(cmd.split()) == 0
+    capsys.readouterr()
+    good = cli._golden_cells(kind, key)
+    assert len(good) == sum(min(i - 1, 6) for i in range(2, 16))
+    bad = dict(good)
+    bad[(4, 2)] += 1
+    monkeypatch.setattr(cli, "_golden_cells", lambda k, kk: bad)
+    assert main(cmd.split()) == 1
+    assert "(4,2)" in capsys.readouterr().err

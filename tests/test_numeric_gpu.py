@@ -363,3 +363,47 @@ def test_rank_deficient_backward_stable(algo):
     assert (torch.linalg.norm(At - Q @ R) / nA).item() <= 1e-12
     eye = torch.eye(q * nb, dtype=torch.float64, device="cuda")
     assert torch.linalg.norm(Q.T @ Q - eye).item() <= 1e-12
+
+
+def test_plan_concurrent_launches_on_two_streams():
+    """A plan is immutable: two factorizations launched at once on two
+    streams (per-launch scratch slots) give the same tiles as sequential
+    runs; a third launch queues behind the first slot."""
+    _need_gpu()
+    p, q, nb = 10, 6, 256
+    plan = Plan(P.build_tree(p, q, "greedy"), nb)
+    As = [torch.from_numpy(np.random.default_rng(40 + s).standard_normal((p * nb, q * nb))).cuda() for s in range(3)]
+    ref = []
+    for A in As:
+        t = plan.alloc()
+        plan.pack(A, t[0])
+        plan.factor(*t)
+        torch.cuda.synchronize()
+        ref.append(t)
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    outs = [plan.alloc() for _ in range(3)]
+    for A, o, s in zip(As, outs, streams):
+        with torch.cuda.stream(s):
+            plan.pack(A, o[0], stream=s)
+            plan.factor(*o, stream=s)
+    torch.cuda.synchronize()
+    for r, o in zip(ref, outs):
+        for a, b in zip(r, o):
+            assert torch.equal(a, b)
+
+
+def test_qr_host_rejects_bad_layout_before_launch():
+    """tqr_qr_host validates the host layout before starting the executor
+    (a column-major pinned A used to hang the device)."""
+    _need_gpu()
+    from paper_1303_3182_b200.engine import tiled_qr_host
+    p, q, nb = 4, 2, 64
+    plan = Plan(P.build_tree(p, q, "greedy"), nb, io=Plan.IO_IN | Plan.IO_OUT)
+    X = torch.randn((q * nb, p * nb), dtype=torch.float64).pin_memory()
+    R = torch.zeros((q * nb, q * nb), dtype=torch.float64).pin_memory()
+    with pytest.raises(ValueError):
+        plan.factor_stream(X.t(), R, plan.stream_buffers())  # column-major view
+    # the public entry point copies such input to row-major and succeeds
+    R_host, _ = tiled_qr_host(X.t(), nb=nb)
+    torch.cuda.synchronize()
+    assert torch.isfinite(R_host).all()

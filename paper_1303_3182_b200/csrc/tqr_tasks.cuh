@@ -323,7 +323,7 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
   double* drow = sm + S::P_DROW;
   double* sbuf = sm + S::P_SBUF;
   double* tau_s = sm + S::P_SC;
-  double* scal_s = tau_s + IB;
+  double* taut_s = tau_s + IB;  // tau = 2 / v^T v of the stored v (T's diagonal)
   double* beta_s = tau_s + 2 * IB;
   const int t = tid;
   unsigned long long tp = (prof && tid == 0) ? ptimer() : 0;
@@ -463,7 +463,6 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
         const double sv = tau * (drowj[v] + scal * D);
         if (tid == 0) {
           tau_s[j] = tau;
-          scal_s[j] = scal;
           beta_s[j] = beta;
         }
         if (tau != 0.0) {
@@ -611,45 +610,85 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
         mark(2);
       }
     }
-    // ---- block Gram G = V^T V (32x32, upper blocks) on DMMA: warp w takes
-    // (m-block, n-block) pairs of the 4x4 block grid with m <= n
+    // ---- block Gram G = V^T V (the 10 upper 8x8 blocks of 32x32) on DMMA.
+    // T's consistency with the stored V sets the orthogonality of the block
+    // reflector (I - V T V^T is orthogonal iff T^-1 + T^-T = V^T V), so G is
+    // accumulated compensated: every 8 rows are formed from zero (two chained
+    // DMMAs) and added error-free (TwoSum) into a hi/lo pair.  The row range
+    // holding the block pair's nonzeros is split in two halves: 20 units on
+    // the 8 warps; the halves' hi/lo are summed in double-double and rounded
+    // once in the combine pass below.
     {
-      const int khi = (nrows + 3) & ~3;
-      for (int pr = warp; pr < 10; pr += NW) {
+      double* Glo = Tp;  // half 0 low parts (Tp is first written after the combine)
+      double* G1 = WP;   // half 1: [pair][hi 64 | lo 64]
+      const int r = lane >> 2, c = lane & 3;
+      for (int u = warp; u < 20; u += NW) {
+        const int pr = u >> 1, half = u & 1;
         const int mb = pr < 4 ? 0 : (pr < 7 ? 1 : (pr < 9 ? 2 : 3));
         const int nbb = pr < 4 ? pr : (pr < 7 ? pr - 3 : (pr < 9 ? pr - 5 : 3));
-        const int klo = (MODE == GE) ? 8 * nbb : 0;  // GE: V's columns 8nbb.. are zero above row 8nbb
-        // T's consistency with the stored V sets the orthogonality of the
-        // block reflector (I - V T V^T orthogonal iff T^-1 + T^-T = V^T V):
-        // the Gram is accumulated compensated (four interleaved chains, each
-        // a double-double hi/lo pair, summed in double-double and rounded
-        // once), so G is V^T V of the stored V to ~1 ulp
-        double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-        double accl[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-        const int r = lane >> 2, c = lane & 3;
-        for (int k = klo; k < khi; k += 16) {
+        // GE: V's columns 8nbb.. are zero above P row 8nbb; TT: column block mb
+        // (the shorter, mb <= nbb) ends at bottom row rb0 + 8mb + 7
+        const int klo = (MODE == GE) ? 8 * nbb : 0;
+        const int khi = (MODE == TT) ? IB + rb0 + 8 * mb + 8 : (nrows + 3) & ~3;
+        const int mid = klo + (((khi - klo) >> 1) & ~7);
+        const int k0 = half ? mid : klo, k1 = half ? khi : mid;
+        double hi[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, lo[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        for (int k = k0; k < k1; k += 16) {
+          double t[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
             const int row = k + 4 * h + c;
-            if (k + 4 * h < khi) {
+            if (k + 4 * h < k1) {
               const double a = vmask_p<NB, MODE>(P[row + (8 * mb + r) * PLD], row, 8 * mb + r);
               const double bv = vmask_p<NB, MODE>(P[row + (8 * nbb + r) * PLD], row, 8 * nbb + r);
-              dmma_comp(acc[h], accl[h], a, bv);
+#ifdef TQR_GRAM_PLAIN
+              dmma(hi[h >> 1], a, bv);
+#else
+              dmma(t[h >> 1], a, bv);
+#endif
             }
           }
+#ifndef TQR_GRAM_PLAIN
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              double s2, er;
+              two_sum(s2, er, hi[q][e], t[q][e]);
+              hi[q][e] = s2;
+              lo[q][e] += er;
+            }
+#endif
         }
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          double hs = acc[0][e], ls = accl[0][e];
-#pragma unroll
-          for (int h = 1; h < 4; ++h) {
-            double t2, er;
-            two_sum(t2, er, hs, acc[h][e]);
-            hs = t2;
-            ls += er + accl[h][e];
+          double s2, er;
+          two_sum(s2, er, hi[0][e], hi[1][e]);
+          const double l2 = er + (lo[0][e] + lo[1][e]);
+          const int idx = (8 * mb + r) + (8 * nbb + 2 * c + e) * IB;
+          if (half == 0) {
+            G[idx] = s2;
+            Glo[idx] = l2;
+          } else {
+            G1[pr * 128 + 2 * lane + e] = s2;
+            G1[pr * 128 + 64 + 2 * lane + e] = l2;
           }
-          G[(8 * mb + r) + (8 * nbb + 2 * c + e) * IB] = hs + ls;
         }
+      }
+      csync();
+      // combine the halves (double-double), round once; tau of each reflector
+      // from its stored v (see the T step)
+      for (int e = tid; e < 640; e += NT) {
+        const int pr = e >> 6, w = e & 63, ln = w >> 1;
+        const int mb = pr < 4 ? 0 : (pr < 7 ? 1 : (pr < 9 ? 2 : 3));
+        const int nbb = pr < 4 ? pr : (pr < 7 ? pr - 3 : (pr < 9 ? pr - 5 : 3));
+        const int i = 8 * mb + (ln >> 2), j = 8 * nbb + 2 * (ln & 3) + (w & 1);
+        const int idx = i + j * IB;
+        double s2, er;
+        two_sum(s2, er, G[idx], G1[pr * 128 + w]);
+        const double gv = s2 + (er + (Glo[idx] + G1[pr * 128 + 64 + w]));
+        G[idx] = gv;
+        if (i == j) taut_s[i] = tau_s[i] != 0.0 ? 2.0 / gv : 0.0;
       }
     }
     csync();
@@ -673,7 +712,12 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
       const int g0 = warp * 8, cc = lane;
       double col[8], tv[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) tv[i] = tau_s[g0 + i] != 0.0 ? 2.0 / G[(g0 + i) * (IB + 1)] : 0.0;
+      for (int i = 0; i < 8; ++i)
+#ifdef TQR_TAU_DLARFG
+        tv[i] = tau_s[g0 + i];
+#else
+        tv[i] = taut_s[g0 + i];
+#endif
 #pragma unroll
       for (int i = 7; i >= 0; --i) {
         double v = 0.0;

@@ -124,6 +124,23 @@ class Plan:
         check(lib().tqr_plan_arrival_units(self._h, C.byref(n), _lib.ptr_i32(out)))
         return [tuple(int(v) for v in out[3 * u:3 * u + 3]) for u in range(n.value)]
 
+    def factor_traced(self, tiles, tg, te, stream=None):
+        """factor() with a per-work-item device timeline (globaltimer stamps
+        at dequeue, dependencies-ready and end, plus the SM id) — returns a
+        DeviceTimeline.  The stamps cost a few store instructions per item."""
+        import numpy as np
+        n = self.info.n_items
+        tr = torch.zeros(4 * n + 64, dtype=torch.int64, device=tiles.device)
+        check(lib().tqr_set_trace(_vp(tr)))
+        try:
+            self.factor(tiles, tg, te, stream)
+            (stream or torch.cuda.current_stream()).synchronize()
+        finally:
+            lib().tqr_set_trace(None)
+        items = np.empty((n, 7), dtype=np.int32)
+        check(lib().tqr_plan_items(self._h, _lib.ptr_i32(items)))
+        return DeviceTimeline(items, tr[:4 * n].view(n, 4).cpu().numpy())
+
     def apply_q(self, trans, tiles, tg, te, c_tiles, c_cols, stream=None):
         check(lib().tqr_apply_q(self._h, int(bool(trans)), _vp(tiles), _vp(tg), _vp(te), _vp(c_tiles),
                                 int(c_cols), _stream_ptr(stream)))
@@ -144,6 +161,60 @@ class Plan:
         A = A.contiguous()
         check(lib().tqr_pack(_vp(A), A.stride(0), 1, _vp(tiles), self.p, cols, self.nb, _stream_ptr(stream)))
         return tiles
+
+
+_KIND = ("GEQRT", "TTQRT", "TSQRT", "UNMQR", "TTMQR", "TSMQR", "PACK", "UNPACK")
+
+
+class DeviceTimeline:
+    """Per-work-item timeline of one executor run: item (kind, slab, i, piv,
+    k, j) ran on SM `sm` from `start` (its dependencies satisfied) to `end`,
+    microseconds from the first dequeue."""
+
+    def __init__(self, items, stamps):
+        t0 = stamps[:, 0].min() if len(stamps) else 0
+        self.items = items
+        self.dequeue = (stamps[:, 0] - t0) / 1e3
+        self.start = (stamps[:, 1] - t0) / 1e3
+        self.end = (stamps[:, 2] - t0) / 1e3
+        self.sm = stamps[:, 3].astype(int)
+
+    @staticmethod
+    def _indices(row):
+        kind, _, i, piv, k, j = (int(x) for x in row[:6])
+        name = _KIND[kind]
+        if name == "GEQRT":
+            return name, (i, k)
+        if name == "UNMQR":
+            return name, (i, k, j)
+        if name in ("TTQRT", "TSQRT"):
+            return name, (i, piv, k)
+        if name in ("PACK", "UNPACK"):
+            return name, (i, j)
+        return name, (i, piv, k, j)
+
+    def gantt_rows(self):
+        """(proc, start, end, kind, i, j, k) rows — the layout of the
+        reference's Schedule.gantt_rows (sched.py:36-43): the first three
+        task indices, padded with "", sorted by (proc, start, kind); proc is
+        the SM, times are in microseconds."""
+        rows = []
+        for r in range(len(self.items)):
+            name, idx = self._indices(self.items[r])
+            idx = list(idx) + [""] * (3 - len(idx))
+            rows.append((int(self.sm[r]), round(float(self.start[r]), 3), round(float(self.end[r]), 3), name,
+                         *idx[:3]))
+        rows.sort(key=lambda x: (x[0], x[1], x[3]))
+        return rows
+
+    def to_csv(self):
+        """Gantt CSV, header proc,start,end,kind,i,j,k (sched.py:45-49)."""
+        lines = ["proc,start,end,kind,i,j,k"]
+        lines += [",".join(str(x) for x in row) for row in self.gantt_rows()]
+        return "\n".join(lines) + "\n"
+
+    def makespan_us(self):
+        return float(self.end.max()) if len(self.end) else 0.0
 
 
 @dataclasses.dataclass

@@ -36,6 +36,52 @@ struct Smem {
   static constexpr size_t BYTES = size_t(END) * sizeof(double);
 };
 
+// 1/sqrt(s) and 1/t for s, t in the normal range: MUFU seed + one cubic
+// Newton step (~1 ulp; no IEEE special-case branches).
+__device__ __forceinline__ double rsqrt_nr(double s) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
+  const double e = fma(-s * y, y, 1.0);
+  return fma(y * e, fma(0.375, e, 0.5), y);
+}
+__device__ __forceinline__ double rcp_nr(double t) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(t));
+  const double e = fma(-t, y, 1.0);
+  return fma(y, fma(e, e, e), y);
+}
+
+// dlarfg's scalars from alpha and xn2 = ||x||^2 (LAPACK dlarfg, with the
+// norm supplied): beta = -sign(alpha) sqrt(alpha^2 + xn2), tau = (beta -
+// alpha) / beta, scal = 1 / (alpha - beta); xn2 == 0 gives tau = 0, beta =
+// alpha.  With r = 1/sqrt(alpha^2 + xn2): tau = 1 + |alpha| r in [1, 2),
+// scal = sign(alpha) r / tau, beta = -sign(alpha) (alpha^2 + xn2) r — one
+// rsqrt and one reciprocal, MUFU seeds + one cubic Newton step each, no IEEE
+// special-case branches (the caller keeps the arguments in the normal range:
+// the panel's scaled path); ~1 ulp.  TQR_L2_IEEE_SCALARS: correctly rounded
+// sqrt and division (measured 5 % slower level-2: 143.6 vs 136.4 us).
+__device__ __forceinline__ void dlarfg_scalars(double alpha, double xn2, double& tau, double& scal, double& beta) {
+  tau = 0.0;
+  scal = 0.0;
+  beta = alpha;
+  if (xn2 != 0.0) {
+#ifndef TQR_L2_IEEE_SCALARS
+    const double sg = copysign(1.0, alpha);
+    const double sq = fma(alpha, alpha, xn2);
+    const double r = rsqrt_nr(sq);
+    tau = fma(fabs(alpha), r, 1.0);
+    scal = sg * r * rcp_nr(tau);
+    beta = -sg * sq * r;
+#else
+    beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
+    // tau = (beta - alpha) / beta and 1 / (alpha - beta) from one division
+    const double am = alpha - beta, rr = 1.0 / (am * beta);
+    tau = -(am * am) * rr;
+    scal = beta * rr;
+#endif
+  }
+}
+
 // After the call lane l holds the warp-wide sum of d[l] (recursive halving).
 __device__ __forceinline__ double warp_reduce_scatter32(double (&d)[32], int lane) {
 #pragma unroll
@@ -406,13 +452,14 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
           for (int c = 0; c < 8; ++c) drowj[c] = rv0[c];
         }
         const bool iv0 = own0 && in_vec(r0w, j), iv1 = own1 && in_vec(r1w, j);
-        const double x0 = iv0 ? rv0[jj] : 0.0, x1 = iv1 ? rv1[jj] : 0.0;
-        double d[8];
+        double x0 = iv0 ? rv0[jj] : 0.0, x1 = iv1 ? rv1[jj] : 0.0;
+        // products of x with the group's 8 columns, reduce-scattered over the
+        // warp (lane L ends with value v(L) = 4*bit4 + 2*bit3 + bit2 summed
+        // over its 32 lanes) into partj[warp][v]
+        auto reduce8 = [&](double xa, double xb) {
+          double d[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) d[c] = (MODE == GE) ? x0 * rv0[c] : fma(x1, rv1[c], x0 * rv0[c]);
-        // reduce-scatter 8 values over the warp: lane L ends with value
-        // v(L) = 4*bit4 + 2*bit3 + bit2 summed over all 32 lanes
-        {
+          for (int c = 0; c < 8; ++c) d[c] = (MODE == GE) ? xa * rv0[c] : fma(xb, rv1[c], xa * rv0[c]);
           const bool u4 = lane & 16;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -433,34 +480,81 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
           d[0] += __shfl_xor_sync(0xffffffffu, d[0], 2);
           d[0] += __shfl_xor_sync(0xffffffffu, d[0], 1);
           if ((lane & 3) == 0) partj[warp * 8 + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = d[0];
-        }
+        };
+        // every warp: lane v (mod 8) sums value v over the warps (the same
+        // tree in every warp, so every warp holds bitwise the same values)
+        const int v = lane & 7;
+        auto sum8 = [&]() {
+          double pw[NW];
+#pragma unroll
+          for (int w = 0; w < NW; ++w) pw[w] = partj[w * 8 + v];
+#pragma unroll
+          for (int h = NW / 2; h >= 1; h >>= 1)
+#pragma unroll
+            for (int w = 0; w < h; ++w) pw[w] += pw[w + h];
+          return pw[0];
+        };
+        // dlarfg scalars (redundantly in every warp, no second barrier).
+        // Common path: alpha^2 + ||x||^2 and every product in range.  Rare
+        // path (CTA-uniform: every warp holds the same sums) — dnrm2-style
+        // scaling: ||x|| tiny/zero or huge, or a product overflowed: the
+        // column's max |x| (one more reduction) gives a power-of-two scale
+        // 2^-ex; the products are redone with x' = 2^-ex x (||x'|| ~ 1,
+        // |x' a| <= |a|, the norm term x' x'), and the scalars follow
+        // dlarfg on the exact scales.
+        reduce8(x0, x1);
         L2P_MARK(0);
         csync();
         L2P_MARK(1);
-        // every warp: lane v (mod 8) sums value v over the warps and computes
-        // the reflector scalars redundantly (no second barrier)
-        const int v = lane & 7;
-        double pw[NW];
-#pragma unroll
-        for (int w = 0; w < NW; ++w) pw[w] = partj[w * 8 + v];
-#pragma unroll
-        for (int h = NW / 2; h >= 1; h >>= 1)
-#pragma unroll
-          for (int w = 0; w < h; ++w) pw[w] += pw[w + h];
-        const double D = pw[0];
-        const double alpha = drowj[jj];
+        const double alpha = drowj[jj];  // row j (written before the barrier)
+        double D = sum8();
         const double xn2 = __shfl_sync(0xffffffffu, D, jj);
-        double tau = 0.0, scal = 0.0, beta = alpha;
-        if (xn2 != 0.0) {
-          beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-          // dlarfg's tau = (beta - alpha) / beta and 1 / (alpha - beta) from
-          // one division
-          const double am = alpha - beta, rr = 1.0 / (am * beta);
-          tau = -(am * am) * rr;
-          scal = beta * rr;
+        // the range check is issued first and resolves beside the scalars'
+        // dependency chain
+        const bool rare = __any_sync(0xffffffffu, !(xn2 >= 0x1p-900 && fma(alpha, alpha, xn2) <= 0x1p900) ||
+                                                      !isfinite(D));
+        // scal_d: 1/(alpha - beta) in the common path; in the scaled path it
+        // multiplies both the products D' (w_c = a_jc + scal D_c) and x'
+        double tau, scal_d, beta;
+        dlarfg_scalars(alpha, xn2, tau, scal_d, beta);
+        if (__builtin_expect(rare, 0)) {
+          double m = fmax(iv0 ? fabs(x0) : 0.0, iv1 ? fabs(x1) : 0.0);
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+          if (lane == 0) sbuf[warp] = m;
+          csync();
+          double amax = 0.0;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) amax = fmax(amax, sbuf[w]);
+          tau = scal_d = 0.0;
+          beta = alpha;
+          if (amax != 0.0) {  // (amax == 0: x = 0 below the diagonal, H = I)
+            const int ex = ilogb(amax);
+            const double xsc = ldexp(1.0, -ex);
+            x0 *= xsc;  // from here on x' (the reflector is v = x' scal_d)
+            x1 *= xsc;
+            if (iv0) rv0[jj] = x0;  // the norm term of the products is x' x'
+            if (iv1) rv1[jj] = x1;
+            reduce8(x0, x1);
+            csync();
+            D = sum8();  // D'_c = 2^-ex D_c
+            const double xn2s = __shfl_sync(0xffffffffu, D, jj);  // ||x'||^2 in [1, rows]
+            if (fabs(alpha) >= ldexp(1.0, ex + 500)) {
+              // ||x|| / |alpha| < 2^-490: dlapy2(alpha, xnorm) = |alpha| in
+              // fp64, so beta = -alpha, tau = 2, scal = 1 / (2 alpha)
+              tau = 2.0;
+              beta = -alpha;
+              scal_d = ldexp(0.5 / alpha, ex);
+            } else {
+              // dlarfg on the scaled column: beta = 2^ex beta', and with
+              // scal = 2^-ex scal': scal D = scal' D', v = x scal = x' scal'
+              dlarfg_scalars(ldexp(alpha, -ex), xn2s, tau, scal_d, beta);
+              beta = ldexp(beta, ex);
+            }
+          }
         }
         L2P_MARK(2);
-        const double sv = tau * (drowj[v] + scal * D);
+        const double sv = tau * (drowj[v] + scal_d * D);
         if (tid == 0) {
           tau_s[j] = tau;
           beta_s[j] = beta;
@@ -470,13 +564,13 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
 #pragma unroll
           for (int c = jj + 1; c < 8; ++c) s[c] = __shfl_sync(0xffffffffu, sv, c);
           if (iv0) {
-            const double xs = x0 * scal;
+            const double xs = x0 * scal_d;
 #pragma unroll
             for (int c = jj + 1; c < 8; ++c) rv0[c] -= s[c] * xs;
             rv0[jj] = xs;
           }
           if (iv1) {
-            const double xs = x1 * scal;
+            const double xs = x1 * scal_d;
 #pragma unroll
             for (int c = jj + 1; c < 8; ++c) rv1[c] -= s[c] * xs;
             rv1[jj] = xs;

@@ -278,13 +278,17 @@ def test_executor_schedule_independent_and_deterministic(p, q, nb, monkeypatch):
 
 
 def _special(kind, p, q, nb):
+    """(A, d): the input and, for the scaled kinds, the column scaling d with
+    A = A0 diag(d), A0 in the normal range (R scales column-wise by d; Q, so
+    V and T, does not) — None for the others."""
     rng = np.random.default_rng(31)
     m, n = p * nb, q * nb
     if kind == "zeros":
-        return np.zeros((m, n))
+        return np.zeros((m, n)), None
     if kind == "identity":
-        return np.eye(m, n)
+        return np.eye(m, n), None
     A = rng.standard_normal((m, n))
+    d = None
     if kind == "zero_cols":  # tau = 0 reflectors (dlarfg with x = 0)
         A[:, [0, 3, 70, n - 1]] = 0.0
     elif kind == "upper":  # already upper triangular: every x below the diagonal is 0
@@ -293,30 +297,73 @@ def _special(kind, p, q, nb):
         A *= 1e100
     elif kind == "tiny":
         A *= 1e-100
-    return A
+    elif kind in ("big200", "tiny200", "graded"):
+        # squares overflow / underflow: the kernels' dnrm2-style scaled path
+        # (LAPACK's dnrm2 / dlapy2 in the replay); power-of-two scales
+        e = {"big200": np.full(n, 664), "tiny200": np.full(n, -664),
+             "graded": np.linspace(-664, 664, n).round()}[kind]
+        d = np.ldexp(1.0, e.astype(int))
+        A = A * d[None, :]
+    elif kind == "tiny_below":
+        # first tile column: normal diagonal and upper part, sub-diagonal
+        # entries whose squares underflow (LAPACK's dnrm2 still sees them:
+        # tau = 2 reflectors); the other columns normal.  (Deeper cascades
+        # of tiny x tiny products reach denormals, where DMMA and LAPACK
+        # round differently — not a meaningful tile-by-tile comparison.)
+        A[:, :nb] = np.triu(A[:, :nb]) + np.tril(A[:, :nb], -1) * 1e-170
+    return A, d
 
 
-@pytest.mark.parametrize("kind", ["zeros", "identity", "zero_cols", "upper", "big", "tiny"])
+def _r_mask(p, q, nb):
+    """Tile-layout mask of the R entries (tile rows i <= j; upper triangle of
+    the diagonal tiles) — the rest holds reflectors."""
+    msk = np.zeros((q, p, nb, nb), dtype=bool)  # [j][i] tiles, column-major inside
+    up = np.triu(np.ones((nb, nb), dtype=bool))  # row <= col, indexed [row][col]
+    for j in range(q):
+        for i in range(min(j + 1, p)):
+            msk[j, i] = up.T if i == j else True  # column-major tile: [col][row]
+    return msk.reshape(-1)
+
+
+def _normalize_tiles(t, d, p, q, nb):
+    """Divide the R entries of a tile array by their column's scale d."""
+    cols = np.broadcast_to(np.arange(q)[:, None, None, None] * nb + np.arange(nb)[None, None, :, None],
+                           (q, p, nb, nb)).reshape(-1)
+    out = t.copy()
+    m = _r_mask(p, q, nb)
+    out[m] = t[m] / d[cols[m]]
+    return out
+
+
+@pytest.mark.parametrize("kind", ["zeros", "identity", "zero_cols", "upper", "big", "tiny", "big200", "tiny200",
+                                  "graded", "tiny_below"])
 @pytest.mark.parametrize("algo,family", [("greedy", "TT"), ("flattree", "TS")])
 def test_special_matrices_match_replay(kind, algo, family):
     """Edge inputs through every kernel path: all-zero / identity / upper-
     triangular matrices (every reflector has x = 0: tau = 0, beta = alpha),
-    zero columns, and scaled matrices (1e+-100: sums of
-    squares stay inside the fp64 range; entries beyond ~1e+-150 would need
-    dnrm2-style scaling, which the kernels do not do) — every tile and T
+    zero columns, scaled matrices 1e+-100 (sums of squares in range), and
+    2^+-664 ~ 1e+-200 and column-graded 2^-664..2^664 (squares overflow /
+    underflow: the panels' dnrm2-style scaled path, against LAPACK's
+    dnrm2 / dlapy2 in the replay — R compared column-scale-normalised), and
+    sub-diagonal entries ~1e-170 under a normal diagonal — every tile and T
     factor against the LAPACK replay."""
     _need_gpu()
     p, q, nb = 6, 3, 64
-    A = _special(kind, p, q, nb)
+    A, d = _special(kind, p, q, nb)
     b = P.build_tree(p, q, algo, family=family)
     plan, res = _run(b, A, nb)
     rp = replay_build(A, b, nb)
-    scale = np.linalg.norm(A)
     t = res.tiles.cpu().numpy()
+    ref = rp.tiles_array()
     assert np.isfinite(t).all()
+    if d is not None:
+        t, ref = _normalize_tiles(t, d, p, q, nb), _normalize_tiles(ref, d, p, q, nb)
+        scale = np.linalg.norm(A / d[None, :])
+    else:
+        scale = np.linalg.norm(A)
+        assert np.linalg.norm(res.R().cpu().numpy() - rp.r()) <= 1e-11 * scale
     # R scales with A; the reflectors (and T) are scale-free
-    assert np.abs(t - rp.tiles_array()).max() <= 1e-11 * max(scale, 1.0)
-    assert np.linalg.norm(res.R().cpu().numpy() - rp.r()) <= 1e-11 * scale
+    assert np.abs(t - ref).max() <= 1e-11 * max(scale, 1.0)
     for which, arr in (("G", res.tg), ("E", res.te)):
         assert np.abs(arr.cpu().numpy() - rp.t_array(which)).max() <= 1e-11, which
 

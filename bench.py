@@ -78,7 +78,7 @@ def config_dict(name, cfg, world=1):
          "family": cfg["family"], "seed": cfg["seed"], "dist": cfg["dist"],
          "tiles": f"{cfg['m'] // nb}x{cfg['n'] // nb}"}
     if name == "c5":
-        d["tree"] = "greedy local trees + binary TT merges"
+        d["tree"] = f"{cfg['algo']} local trees + binary TT merges"
         d["parallelism"] = f"block rows over {world} GPU(s), NCCL p2p R merges"
     else:
         d["parallelism"] = "1 GPU, persistent dataflow executor"
@@ -386,7 +386,7 @@ def run_c5(args, name, cfg):
         """(ms per step, R block on rank 0, backend) for G shards."""
         P = p // G
         A = torch.from_numpy(A_host).to(dev)
-        be = dist.GpuBackend(P, q, nb, dev)
+        be = dist.GpuBackend(P, q, nb, dev, algo=cfg["algo"])
 
         def step():
             return dist.tall_skinny_qr(A, be, rank_, G, comm)
@@ -571,6 +571,7 @@ def parse_args(argv=None):
     ap.add_argument("--no-single", action="store_true", help="N>1: skip rank 0's one-GPU C5 point")
     ap.add_argument("--ref-step-s", type=float, default=3.0, help="CPU replay window per step (s)")
     ap.add_argument("--dry", action="store_true", help="CPU launcher check: ranks, gloo exchange, no kernels")
+    ap.add_argument("--tree", default=None, help="override the workload's elimination tree (e.g. asap, grasap)")
     args = ap.parse_args(argv)
     if args.config is None:
         args.config = "c3" if args.gpus == 1 else "c5"
@@ -582,6 +583,8 @@ def main():
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn(args))
     name, cfg = args.config, CONFIGS[args.config]
+    if args.tree:
+        cfg = dict(cfg, algo=args.tree)
     if args.impl == "reference":
         return run_reference(args, name, cfg)
     if args.dry:

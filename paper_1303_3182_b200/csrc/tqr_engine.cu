@@ -452,6 +452,7 @@ cudaError_t run(const DevSched& d, int nb, bool apply, bool transT, const double
   auto launch = [&]() -> cudaError_t {
     switch (nb) {
       TQR_RUN_NB(64)
+      TQR_RUN_NB(128)
       TQR_RUN_NB(256)
     }
     return cudaErrorInvalidValue;
@@ -479,7 +480,7 @@ int tqr_plan_create_io(const tqr_build* hb, int nb, int ib, int io, tqr_plan** o
     if (!hb || !hb->b) throw tqr::ValueError("null build");
     const tqr::Build& b = *hb->b;
     if (!b.keep_trace) throw tqr::ValueError("plan needs a build made with keep_trace=True");
-    if (nb != 64 && nb != 256) throw tqr::ValueError("nb must be 64 or 256");
+    if (nb != 64 && nb != 128 && nb != 256) throw tqr::ValueError("nb must be 64, 128 or 256");
     if (ib != IB) throw tqr::ValueError("ib must be 32");
     auto* P = new tqr_plan;
     try {

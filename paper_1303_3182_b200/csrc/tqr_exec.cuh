@@ -387,6 +387,9 @@ cudaError_t launch_exec(const DevView& d, const double* vtiles, double* tiles, d
 TQR_DECLARE_LAUNCH(64, true, false)
 TQR_DECLARE_LAUNCH(64, true, true)
 TQR_DECLARE_LAUNCH(64, false, true)
+TQR_DECLARE_LAUNCH(128, true, false)
+TQR_DECLARE_LAUNCH(128, true, true)
+TQR_DECLARE_LAUNCH(128, false, true)
 TQR_DECLARE_LAUNCH(256, true, false)
 TQR_DECLARE_LAUNCH(256, true, true)
 TQR_DECLARE_LAUNCH(256, false, true)

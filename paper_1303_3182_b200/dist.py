@@ -4,8 +4,8 @@ Block-row partition: rank r owns tile rows [r*P+1, (r+1)*P] of a p x q tile
 matrix (P = p/G).  Each rank factors its shard with the reference's Greedy
 tree (coarse_schedule, qr.py:254-297) — no communication.  Then log2(G)
 rounds of binary TT merges: in round s (stride 2^s) rank b = a + stride
-sends its q x q-tile R factor to rank a (one NCCL point-to-point message of
-q*q tiles), and rank a eliminates the stacked [R_a; R_b] column by column
+sends the upper block triangle of its q x q-tile R factor to rank a (one
+NCCL point-to-point message of q(q+1)/2 tiles), and rank a eliminates the stacked [R_a; R_b] column by column
 with TTQRT / TTMQR / GEQRT / UNMQR, pairing rows as soon as they are ready
 under the device cost model (the Asap event rule, qr.py:551-583; the
 round-1 Greedy-style pairing is kept as merge_pairs_greedy — its critical
@@ -187,7 +187,7 @@ def merge_rounds(G):
 class GpuBackend:
     """Local factorization and merges with the libtqr engine."""
 
-    def __init__(self, P, q, nb, device):
+    def __init__(self, P, q, nb, device, algo="greedy"):
         import torch
 
         from .engine import Plan
@@ -195,7 +195,7 @@ class GpuBackend:
 
         self.torch = torch
         self.P, self.q, self.nb, self.dev = P, q, nb, device
-        self.local_plan = Plan(build_tree(P, q, "greedy"), nb)
+        self.local_plan = Plan(build_tree(P, q, algo), nb)
         kinds, idx = merge_trace(q)
         h = C.c_void_p()
         _lib.check(_lib.lib().tqr_trace_build(2 * q, q, kinds.ctypes.data_as(_lib.i8p), _lib.ptr_i32(idx),
@@ -283,27 +283,43 @@ class GpuBackend:
         return R
 
 
+def _upper_tiles(q):
+    """Flat indices of the R tiles (i <= j) in a [q cols][q tiles] block."""
+    return [j * q + i for j in range(q) for i in range(j + 1)]
+
+
 def tall_skinny_qr(A_local, backend, rank, world, dist=None, keep_q=False):
     """Factor the block rows A_local on every rank; rank 0 returns the final
     q x q-tile R block (others return None).  `dist` is torch.distributed
-    (send/recv of the R block; NCCL on GPUs, gloo in the CPU tests).
-    A_local on the host (page-locked, GpuBackend) streams in while the local
-    factorization runs.  keep_q keeps every merge's factors on the
+    (send/recv of the R block; NCCL on GPUs, gloo in the CPU tests).  Only
+    the q(q+1)/2 tiles of R's upper block triangle travel (18 MiB at q = 8
+    instead of 32): the merge trace never reads a tile below the block
+    diagonal.  A_local on the host (page-locked, GpuBackend) streams in while
+    the local factorization runs.  keep_q keeps every merge's factors on the
     receiving rank for tall_skinny_apply_q (the local factors stay in the
     backend until its next factorization)."""
     if getattr(A_local, "is_cuda", True) or not hasattr(backend, "factor_local_host"):
         r = backend.factor_local(A_local)
     else:
         r = backend.factor_local_host(A_local)
+    rounds = merge_rounds(world)
+    if not rounds:
+        return r if rank == 0 else None
+    import torch
+    q = backend.q
+    t2 = r.numel() // (q * q)
+    up = torch.tensor(_upper_tiles(q), dtype=torch.long, device=r.device)
     recv = None
-    for stride, pairs in merge_rounds(world):
+    for stride, pairs in rounds:
         for a, b in pairs:
             if rank == b:
-                dist.send(r, dst=a)
+                dist.send(r.view(q * q, t2).index_select(0, up), dst=a)
             elif rank == a:
                 if recv is None:
-                    recv = r.new_empty(r.shape)
-                dist.recv(recv, src=b)
+                    recv = r.new_zeros(r.shape)
+                    packed = r.new_empty((len(up), t2))
+                dist.recv(packed, src=b)
+                recv.view(q * q, t2).index_copy_(0, up, packed)
                 r = backend.merge(r, recv, key=stride) if keep_q else backend.merge(r, recv)
     return r if rank == 0 else None
 

@@ -231,32 +231,45 @@ class StreamBuffers:
 
 
 class TiledQR:
-    """Result of a tiled QR: factored tiles (R + reflectors) and T factors."""
+    """Result of a tiled QR: factored tiles (R + reflectors) and T factors.
+    `shape` is the caller's m x n when the matrix was zero-padded to whole
+    tiles (R, Q and apply_q then answer for the unpadded matrix)."""
 
-    def __init__(self, plan: Plan, tiles, tg, te):
+    def __init__(self, plan: Plan, tiles, tg, te, shape=None):
         self.plan, self.tiles, self.tg, self.te = plan, tiles, tg, te
+        self.shape = tuple(shape) if shape is not None else (plan.m, plan.n)
 
     @property
     def build(self):
         return self.plan.build
 
     def R(self):
-        return self.plan.extract_r(self.tiles)
+        n = self.shape[1]
+        R = self.plan.extract_r(self.tiles)
+        return R if n == self.plan.n else R[:n, :n].contiguous()
 
     def apply_q(self, C_mat, trans=False):
-        """Q @ C (trans=False) or Q^T @ C (trans=True) for an m x c device matrix."""
+        """Q @ C (trans=False) or Q^T @ C (trans=True) for an m x c device
+        matrix (m the factored matrix's rows; zero-padded to whole tiles
+        internally)."""
         P = self.plan
-        cols = C_mat.shape[1] // P.nb
-        assert C_mat.shape == (P.m, cols * P.nb)
+        m, c = C_mat.shape
+        assert m == self.shape[0], (C_mat.shape, self.shape)
+        cols = -(-c // P.nb)
+        if (m, c) != (P.m, cols * P.nb):
+            Cp = torch.zeros((P.m, cols * P.nb), dtype=torch.float64, device=C_mat.device)
+            Cp[:m, :c] = C_mat
+            C_mat = Cp
         ct = P.pack_cols(C_mat, cols)
         P.apply_q(trans, self.tiles, self.tg, self.te, ct, cols)
-        return P.unpack(ct, cols)
+        out = P.unpack(ct, cols)
+        return out if out.shape == (m, c) else out[:m, :c].contiguous()
 
     def Q(self):
         """Explicit m x n Q (reverse reflector replay on [I; 0])."""
-        P = self.plan
-        E = torch.zeros((P.m, P.n), dtype=torch.float64, device=self.tiles.device)
-        E[:P.n].fill_diagonal_(1.0)
+        m, n = self.shape
+        E = torch.zeros((m, n), dtype=torch.float64, device=self.tiles.device)
+        E[:n].fill_diagonal_(1.0)
         return self.apply_q(E, trans=False)
 
 
@@ -266,34 +279,59 @@ def tiled_qr_host(A_host, R_host=None, nb=256, algo="greedy", family="TT", bs=No
     factorization (PACK/UNPACK work items, tqr_qr_host).  A_host: fp64
     m x n row-major (pinned for full overlap); returns (R_host, TiledQR)."""
     A_host = torch.as_tensor(A_host, dtype=torch.float64)
-    if not (A_host.is_pinned() and A_host.stride(1) == 1 and A_host.stride(0) >= A_host.shape[1]):
-        A_host = A_host.contiguous().pin_memory()  # row-major, unit column stride
     m, n = A_host.shape
+    if m < n:
+        raise ValueError(f"need m >= n (got {m}x{n})")
+    p, q = -(-m // nb), -(-n // nb)
+    shape = (m, n)
+    if (p * nb, q * nb) != (m, n):  # zero-pad to whole tiles (see tiled_qr)
+        Ap = torch.zeros((p * nb, q * nb), dtype=torch.float64).pin_memory()
+        Ap[:m, :n] = A_host
+        A_host = Ap
+    elif not (A_host.is_pinned() and A_host.stride(1) == 1 and A_host.stride(0) >= A_host.shape[1]):
+        A_host = A_host.contiguous().pin_memory()  # row-major, unit column stride
     if plan is None:
-        build = build_tree(m // nb, n // nb, algo, family=family, bs=bs, grasap_i=grasap_i)
+        build = build_tree(p, q, algo, family=family, bs=bs, grasap_i=grasap_i)
         plan = Plan(build, nb, io=Plan.IO_IN | Plan.IO_OUT)
-    if R_host is None:
-        R_host = torch.zeros((n, n), dtype=torch.float64).pin_memory()
+    R_pad = R_host if (R_host is not None and shape[1] == q * nb) else None
+    if R_pad is None:
+        R_pad = torch.zeros((q * nb, q * nb), dtype=torch.float64).pin_memory()
     if buffers is None:
         buffers = plan.stream_buffers()
-    plan.factor_stream(A_host, R_host, buffers)
-    return R_host, TiledQR(plan, buffers.tiles, buffers.tg, buffers.te)
+    plan.factor_stream(A_host, R_pad, buffers)
+    if R_pad is not R_host:
+        if R_host is None:
+            R_host = R_pad[:n, :n].clone()
+        else:
+            R_host.copy_(R_pad[:n, :n])
+    return R_host, TiledQR(plan, buffers.tiles, buffers.tg, buffers.te, shape)
 
 
 def tiled_qr(A, nb=256, ib=32, algo="greedy", family="TT", bs=None, grasap_i=1, elim=None, plan=None):
-    """Tiled QR of an m x n fp64 matrix (m = p nb, n = q nb, p >= q).
+    """Tiled QR of an m x n fp64 matrix, m >= n, as p x q tiles of nb x nb
+    (nb in {64, 128, 256}).  A matrix that is not a whole number of tiles is
+    zero-padded to p = ceil(m/nb), q = ceil(n/nb) (zero rows below and zero
+    columns to the right leave R's leading n x n block and Q's leading m x n
+    block unchanged: the reflectors never touch zero rows, and zero columns
+    give tau = 0).
 
     The elimination tree is ``build_tree(p, q, algo, family, bs, grasap_i)``
-    or the given EliminationList ``elim`` (validated, tiled_build).  A on the
-    host is copied to the current device.  Returns a TiledQR.
+    or the given elimination list ``elim`` (this package's or the
+    reference's; validated, tiled_build).  A on the host is copied to the
+    current device.  Returns a TiledQR.
     """
     if not torch.cuda.is_available():
         raise RuntimeError("tiled QR needs a CUDA device (no CPU fallback)")
     A = torch.as_tensor(A, dtype=torch.float64)
     m, n = A.shape
-    if m % nb or n % nb:
-        raise ValueError(f"matrix {m}x{n} is not a whole number of {nb}x{nb} tiles")
-    p, q = m // nb, n // nb
+    if m < n:
+        raise ValueError(f"need m >= n (got {m}x{n})")
+    p, q = -(-m // nb), -(-n // nb)
+    shape = (m, n)
+    if (p * nb, q * nb) != (m, n):
+        Ap = torch.zeros((p * nb, q * nb), dtype=torch.float64, device=A.device)
+        Ap[:m, :n] = A
+        A = Ap
     if plan is None:
         if elim is not None:
             if not (hasattr(elim, "p") and hasattr(elim, "q") and hasattr(elim, "__iter__")):
@@ -309,4 +347,4 @@ def tiled_qr(A, nb=256, ib=32, algo="greedy", family="TT", bs=None, grasap_i=1, 
     tiles, tg, te = plan.alloc(A.device)
     plan.pack(A, tiles)
     plan.factor(tiles, tg, te)
-    return TiledQR(plan, tiles, tg, te)
+    return TiledQR(plan, tiles, tg, te, shape)

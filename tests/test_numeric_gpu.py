@@ -454,3 +454,70 @@ def test_qr_host_rejects_bad_layout_before_launch():
     R_host, _ = tiled_qr_host(X.t(), nb=nb)
     torch.cuda.synchronize()
     assert torch.isfinite(R_host).all()
+
+
+@pytest.mark.parametrize("algo,family,bs,p,q", [("greedy", "TT", None, 5, 3), ("fibonacci", "TT", None, 4, 4),
+                                                ("flattree", "TS", None, 4, 2), ("plasmatree", "TT", 2, 6, 3),
+                                                ("grasap", "TT", None, 5, 3)])
+def test_nb128_vs_replay(algo, family, bs, p, q):
+    """nb = 128 tiles: every tile and T factor against the LAPACK replay."""
+    _need_gpu()
+    A = np.random.default_rng(12).standard_normal((p * 128, q * 128))
+    b = P.build_tree(p, q, algo, family=family, bs=bs)
+    plan, res = _run(b, A, 128)
+    _compare_tiles(res, replay_build(A, b, 128), np.linalg.norm(A), (algo, family, 128))
+
+
+@pytest.mark.parametrize("m,n,nb,algo", [(1000, 600, 256, "greedy"), (700, 700, 128, "fibonacci"),
+                                         (300, 65, 64, "greedy"), (8000, 400, 256, "greedy"),
+                                         (513, 257, 128, "plasmatree")])
+def test_padded_shapes(m, n, nb, algo):
+    """Shapes that are not whole tiles are zero-padded: R equals cuSOLVER's
+    after row-sign normalisation, ||A - QR|| and ||Q^T Q - I|| on the m x n
+    Q, and the host-to-host path gives the same R."""
+    _need_gpu()
+    from paper_1303_3182_b200.engine import tiled_qr_host
+    A = np.random.default_rng(13).standard_normal((m, n))
+    At = torch.from_numpy(A).cuda()
+    res = tiled_qr(At, nb=nb, algo=algo, bs=2 if algo == "plasmatree" else None)
+    R = res.R()
+    assert R.shape == (n, n)
+    Q = res.Q()
+    assert Q.shape == (m, n)
+    nA = torch.linalg.norm(At).item()
+    assert torch.linalg.norm(At - Q @ R).item() / nA <= 1e-13
+    assert torch.linalg.norm(Q.T @ Q - torch.eye(n, dtype=torch.float64, device="cuda")).item() <= 1e-12
+    assert _r_vs_cusolver(At, R) <= 1e-11 * nA
+    QtA = res.apply_q(At, trans=True)
+    assert torch.linalg.norm(QtA[:n] - R).item() <= 1e-12 * nA
+    R_host, _ = tiled_qr_host(torch.from_numpy(A), nb=nb, algo=algo, bs=2 if algo == "plasmatree" else None)
+    assert torch.equal(R_host, R.cpu())
+
+
+@pytest.mark.parametrize("algo,p,q,nb", [("asap", 64, 64, 256), ("grasap", 64, 64, 256),
+                                         ("asap", 1024, 8, 256), ("grasap", 1024, 8, 256)])
+def test_asap_grasap_at_scale(algo, p, q, nb):
+    """Asap / GrASAP trees (qr.py:551-611) at C3 scale (64 x 64 tiles) and at
+    C5-shard scale (1024 x 8 tiles, the per-rank work at 8 GPUs): the
+    schedule is the reference's (cp from the C++ port, pinned by the golden
+    fixtures), R equals cuSOLVER's after row-sign normalisation, backward
+    error and orthogonality at the north_star bounds."""
+    _need_gpu()
+    A = torch.randn((p * nb, q * nb), dtype=torch.float64, device="cuda",
+                    generator=torch.Generator(device="cuda").manual_seed(p + q))
+    res = tiled_qr(A, nb=nb, algo=algo)
+    assert P.verify_weight(res.build)
+    R = res.R()
+    nA = torch.linalg.norm(A).item()
+    assert _r_vs_cusolver(A, R) <= 1e-11 * nA
+    if p * q <= 64 * 64 and p == q:
+        Q = res.Q()
+        assert torch.linalg.norm(A - Q @ R).item() / nA <= 1e-12
+        n = R.shape[0]
+        assert torch.linalg.norm(Q.T @ Q - torch.eye(n, dtype=torch.float64, device="cuda")).item() <= 1e-12
+    else:
+        # tall: Q^T A = [R; 0]
+        QtA = res.apply_q(A, trans=True)
+        n = R.shape[0]
+        assert torch.linalg.norm(QtA[:n] - R).item() / nA <= 1e-12
+        assert torch.linalg.norm(QtA[n:]).item() / nA <= 1e-12

@@ -3,7 +3,7 @@
 Workloads (BASELINE.json configs; synthetic seeded inputs, no datasets):
   c3  16384 x 16384, nb=256, Greedy/TT, N(0,1) seed 2          (default, N=1)
   c4   8192 x 4096,  nb=256, Fibonacci/TT, U diag(s) V^T seed 3
-  c5  2,097,152 x 2048, nb=256, Greedy local trees + binary TT merges,
+  c5  2,097,152 x 2048, nb=256, Greedy local trees + TT merge of the R factors,
       U(-1,1) seed 4, block rows sharded over the ranks         (default, N>1)
   c1     512 x 256,  nb=64,  Greedy/TT, N(0,1) seed 0
 
@@ -78,8 +78,8 @@ def config_dict(name, cfg, world=1):
          "family": cfg["family"], "seed": cfg["seed"], "dist": cfg["dist"],
          "tiles": f"{cfg['m'] // nb}x{cfg['n'] // nb}"}
     if name == "c5":
-        d["tree"] = f"{cfg['algo']} local trees + binary TT merges"
-        d["parallelism"] = f"block rows over {world} GPU(s), NCCL p2p R merges"
+        d["tree"] = f"{cfg['algo']} local trees + TT merges of the R factors"
+        d["parallelism"] = f"block rows over {world} GPU(s), NCCL p2p R blocks to rank 0, one TT merge"
     else:
         d["parallelism"] = "1 GPU, persistent dataflow executor"
     bytes_in = 8 * cfg["m"] * cfg["n"]
@@ -365,7 +365,8 @@ def profile_traffic(workload):
 
 def run_c5(args, name, cfg):
     """C5 on N ranks (N=1: the whole matrix on one GPU): local Greedy trees +
-    binary TT merges (paper_1303_3182_b200.dist); device time, max over ranks."""
+    a TT merge of the R factors (one gather merge on rank 0, or binary
+    rounds; paper_1303_3182_b200.dist); device time, max over ranks."""
     import ctypes as C
 
     import torch
@@ -389,7 +390,7 @@ def run_c5(args, name, cfg):
         be = dist.GpuBackend(P, q, nb, dev, algo=cfg["algo"])
 
         def step():
-            return dist.tall_skinny_qr(A, be, rank_, G, comm)
+            return dist.tall_skinny_qr(A, be, rank_, G, comm, merge=args.merge)
 
         for _ in range(args.warmup):
             step()
@@ -446,7 +447,8 @@ def run_c5(args, name, cfg):
         ne = max(1, min(args.steps, 2))
 
         def e2e_step():
-            o = dist.tall_skinny_qr(host if reg else host.to(dev), be, rank, world, td if world > 1 else None)
+            o = dist.tall_skinny_qr(host if reg else host.to(dev), be, rank, world, td if world > 1 else None,
+                                    merge=args.merge)
             if rank == 0:
                 R_host.copy_(be.r_matrix(o), non_blocking=True)
 
@@ -485,8 +487,10 @@ def run_c5(args, name, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(name, cfg, world),
-            # per step on rank 0: pack + executor, then one merge executor per round
-            "gpu_launches": (2 + len(dist.merge_rounds(world))) * args.steps,
+            # per step on rank 0: pack + executor, then the merge executor(s)
+            "gpu_launches": (2 + (min(1, world - 1) if args.merge == "gather" else len(dist.merge_rounds(world))))
+            * args.steps,
+            "merge": args.merge,
             "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 3),
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
                          "kernel": "exec_kernel (local factorization + merges)",
@@ -521,8 +525,9 @@ def run_dry(args, name, cfg):
 
     class DryBackend:
         def __init__(self):
+            self.q = q
             self.build = P.build_tree(p // world, q, "greedy")
-            self.merge_kinds, _ = dist.merge_trace(q)
+            self.merge_kinds, _ = dist.merge_trace(q, world if args.merge == "gather" else 2)
 
         def factor_local(self, A_local):
             return torch.full((q * q * 4,), float(rank))
@@ -530,9 +535,12 @@ def run_dry(args, name, cfg):
         def merge(self, r_a, r_b, key=None):
             return r_a + r_b
 
+        def merge_many(self, rs, key=None):
+            return sum(rs[1:], rs[0])
+
     be = DryBackend()
     t0 = time.perf_counter()
-    out = dist.tall_skinny_qr(None, be, rank, world, td if world > 1 else None)
+    out = dist.tall_skinny_qr(None, be, rank, world, td if world > 1 else None, merge=args.merge)
     dt = time.perf_counter() - t0
     if rank == 0:
         print(json.dumps({"metric": METRIC, "value": None, "unit": "GFLOP/s", "n_gpus": world, "dry": True,
@@ -572,6 +580,8 @@ def parse_args(argv=None):
     ap.add_argument("--ref-step-s", type=float, default=3.0, help="CPU replay window per step (s)")
     ap.add_argument("--dry", action="store_true", help="CPU launcher check: ranks, gloo exchange, no kernels")
     ap.add_argument("--tree", default=None, help="override the workload's elimination tree (e.g. asap, grasap)")
+    ap.add_argument("--merge", default="gather", choices=["gather", "binary"],
+                    help="C5 R merges: one gather merge on rank 0, or log2 N binary rounds")
     args = ap.parse_args(argv)
     if args.config is None:
         args.config = "c3" if args.gpus == 1 else "c5"

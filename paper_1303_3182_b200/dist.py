@@ -57,41 +57,50 @@ def merge_pairs_greedy(q, row_a, rows_b):
     return out
 
 
-def merge_pairs(q, row_a, rows_b, cost=None):
-    """Eliminations merging R_a (rows row_a(k)) with R_b (rows rows_b(i)),
-    paired as soon as possible (the event rule of the reference's Asap,
-    qr.py:551-583, under the device cost model): per column k the live
-    rows are R_a's row k, R_b's row k (both ready at once: untouched by
-    earlier columns) and the rows eliminated in column k-1 (ready after
-    their TTMQR on column k and the GEQRT that re-triangularizes it).  The
-    two earliest-ready rows pair: R_a's row survives when it is one of them
-    (it ends as R's row k), otherwise the lower merge row survives; the
-    survivor is ready again after the TTQRT.  Entries are emitted in
+def merge_pairs_multi(q, rows_of, cost=None):
+    """Eliminations merging G upper block-triangular R factors (block g's
+    row i is rows_of[g](i); block 0 holds the result), paired as soon as
+    possible (the event rule of the reference's Asap, qr.py:551-583, under
+    the device cost model): per column k the live rows are row k of every
+    block (ready at once: untouched by earlier columns) and the rows
+    eliminated in column k-1 (ready after their TTMQR on column k and the
+    GEQRT that re-triangularizes it).  The two earliest-ready rows pair, the
+    lower merge row (block 0's row k when involved: it ends as R's row k)
+    survives and is ready again after the TTQRT.  Entries are emitted in
     simulated start order (ties: row numbers), a valid list order."""
     import heapq
 
     c = cost or MERGE_COST
+    G = len(rows_of)
     ev, carry = [], []
     for k in range(1, q + 1):
-        live = [(0, k), (0, q + k)] + carry  # (ready time, merge row)
+        live = [(0, g * q + k) for g in range(G)] + carry  # (ready time, merge row)
         carry = []
         heapq.heapify(live)
         while len(live) > 1:
             t1, r1 = heapq.heappop(live)
             t2, r2 = heapq.heappop(live)
             s = max(t1, t2)
-            piv, tgt = (r1, r2) if (r1 == k or (r2 != k and r1 < r2)) else (r2, r1)
+            piv, tgt = (r1, r2) if r1 < r2 else (r2, r1)
             ev.append((s, tgt, piv, k))
             heapq.heappush(live, (s + c["ttqrt"], piv))
             carry.append((s + c["ttqrt"] + c["ttmqr"] + c["geqrt"], tgt))
         assert live[0][1] == k
     ev.sort()
-    row = lambda r: row_a(r) if r <= q else rows_b(r - q)  # noqa: E731
+    row = lambda r: rows_of[(r - 1) // q]((r - 1) % q + 1)  # noqa: E731
     return [ElimEntry(row(t), row(v), k) for _, t, v, k in ev]
 
 
-def composite_list(p, q, G):
-    """Global elimination list of G local Greedy trees + binary merges."""
+def merge_pairs(q, row_a, rows_b, cost=None):
+    """Two-block merge_pairs_multi: R_a (rows row_a(k)) with R_b."""
+    return merge_pairs_multi(q, [row_a, rows_b], cost)
+
+
+def composite_list(p, q, G, merge="binary"):
+    """Global elimination list of G local Greedy trees + the merges:
+    log2 G rounds of binary merges (merge="binary", SURVEY.md App. B.2 with
+    Asap pairing) or one gather merge of all G R factors on block 0
+    (merge="gather")."""
     if p % G:
         raise ValueError("p must be a multiple of the number of shards")
     P = p // G
@@ -101,6 +110,10 @@ def composite_list(p, q, G):
     entries = []
     for s in range(G):
         entries += [ElimEntry(e.i + s * P, e.piv + s * P, e.k) for e in local]
+    if merge == "gather":
+        if G > 1:
+            entries += merge_pairs_multi(q, [lambda i, g=g: g * P + i for g in range(G)])
+        return EliminationList(p, q, entries).with_steps()
     stride = 1
     while stride < G:
         for a in range(0, G, 2 * stride):
@@ -111,14 +124,14 @@ def composite_list(p, q, G):
     return EliminationList(p, q, entries).with_steps()
 
 
-def merge_trace(q):
-    """Kernel trace of one merge on the stacked 2q x q tile matrix
-    [R_a; R_b] (rows 1..q = R_a, q+1..2q = R_b): the TT bundle of each merge
-    elimination (qr.py:494-502) — TTQRT, TTMQR for j > k, and the eliminated
-    row re-triangularized in column k+1 (GEQRT + UNMQR).  Tiles below the
-    block diagonal are structurally zero and never touched."""
+def merge_trace(q, G=2):
+    """Kernel trace of one merge on the stacked G q x q tile matrix
+    [R_0; R_1; ...] (rows g q + 1 .. g q + q = R_g): the TT bundle of each
+    merge elimination (qr.py:494-502) — TTQRT, TTMQR for j > k, and the
+    eliminated row re-triangularized in column k+1 (GEQRT + UNMQR).  Tiles
+    below the block diagonals are structurally zero and never touched."""
     kinds, idx = [], []
-    for e in merge_pairs(q, lambda k: k, lambda i: q + i):
+    for e in merge_pairs_multi(q, [lambda i, g=g: g * q + i for g in range(G)]):
         kinds.append(KIND_ID[TTQRT])
         idx.append((e.i, e.piv, e.k, -1))
         for j in range(e.k + 1, q + 1):
@@ -133,7 +146,7 @@ def merge_trace(q):
     return np.asarray(kinds, dtype=np.int8), np.asarray(idx, dtype=np.int32).reshape(-1, 4)
 
 
-def emulate(A, G, nb, backend_cls=None, device=None, keep=False):
+def emulate(A, G, nb, backend_cls=None, device=None, keep=False, merge="binary"):
     """Single-device emulation of tall_skinny_qr with G shards (same local
     trees and merge order; the exchange is a device copy).  For tests.
     keep=True gives every shard its own backend (the local factors stay for
@@ -145,6 +158,10 @@ def emulate(A, G, nb, backend_cls=None, device=None, keep=False):
     rs = []
     for s in range(G):
         rs.append(bes[s].factor_local(A[s * P * nb:(s + 1) * P * nb]).clone())
+    if merge == "gather":
+        if G > 1:
+            rs[0] = bes[0].merge_many(rs, key="gather" if keep else None).clone()
+        return (bes if keep else bes[0]), rs[0]
     for stride, pairs in merge_rounds(G):
         for a, b in pairs:
             m = bes[a].merge(rs[a], rs[b], key=stride) if keep else bes[a].merge(rs[a], rs[b])
@@ -152,7 +169,7 @@ def emulate(A, G, nb, backend_cls=None, device=None, keep=False):
     return (bes if keep else bes[0]), rs[0]
 
 
-def emulate_apply_q(bes, C, trans):
+def emulate_apply_q(bes, C, trans, merge="binary"):
     """Q^T C (trans) or Q C of an emulate(..., keep=True) factorization; C is
     the global m x c device matrix, split by the same block rows."""
     G = len(bes)
@@ -162,6 +179,12 @@ def emulate_apply_q(bes, C, trans):
     rounds = merge_rounds(G)
     if trans:
         cs = [be.apply_local(c, True) for be, c in zip(bes, cs)]
+    if merge == "gather":
+        if G > 1:
+            outs = bes[0].apply_merge_many("gather", [c[:h] for c in cs], trans)
+            for c, o in zip(cs, outs):
+                c[:h].copy_(o)
+        rounds = []
     for stride, pairs in (rounds if trans else rounds[::-1]):
         for a, b in pairs:
             ta, tb = bes[a].apply_merge(stride, cs[a][:h], cs[b][:h], trans)
@@ -196,16 +219,9 @@ class GpuBackend:
         self.torch = torch
         self.P, self.q, self.nb, self.dev = P, q, nb, device
         self.local_plan = Plan(build_tree(P, q, algo), nb)
-        kinds, idx = merge_trace(q)
-        h = C.c_void_p()
-        _lib.check(_lib.lib().tqr_trace_build(2 * q, q, kinds.ctypes.data_as(_lib.i8p), _lib.ptr_i32(idx),
-                                              len(kinds), C.byref(h)))
-        mb = QrBuild.__new__(QrBuild)
-        mb.__dict__.update(p=2 * q, q=q, family="TT", keep_trace=True, _h=h, record_updates=False)
-        self._merge_build = mb
-        self.merge_plan = Plan(mb, nb)
         self.tiles, self.tg, self.te = self.local_plan.alloc(device)
-        self.mtiles, self.mtg, self.mte = self.merge_plan.alloc(device)
+        self._merges = {}  # G stacked R blocks -> (plan, tiles, tg, te)
+        self._merge_setup(2)
         t2 = nb * nb
         self.rbuf = torch.empty(q * q * t2, dtype=torch.float64, device=device)
         self.merge_factors = {}  # merge key (round stride) -> (tiles, tg, te)
@@ -241,18 +257,40 @@ class GpuBackend:
         self.rbuf.view(self.q, self.q * t2).copy_(src)
         return self.rbuf
 
-    def merge(self, r_a, r_b, key=None):
-        """[R_a; R_b] -> merged R (q x q tiles, written into r_a).  With a
-        key the merge's reflectors and T factors are kept for apply_merge."""
-        t2 = self.nb * self.nb
-        m = self.mtiles.view(self.q, 2 * self.q * t2)
-        m[:, :self.q * t2].copy_(r_a.view(self.q, self.q * t2))
-        m[:, self.q * t2:].copy_(r_b.view(self.q, self.q * t2))
-        self.merge_plan.factor(self.mtiles, self.mtg, self.mte)
+    def _merge_setup(self, G):
+        """Plan + buffers of the merge of G stacked R blocks (merge_trace)."""
+        if G not in self._merges:
+            from .engine import Plan
+            from .qr import QrBuild
+            kinds, idx = merge_trace(self.q, G)
+            h = C.c_void_p()
+            _lib.check(_lib.lib().tqr_trace_build(G * self.q, self.q, kinds.ctypes.data_as(_lib.i8p),
+                                                  _lib.ptr_i32(idx), len(kinds), C.byref(h)))
+            mb = QrBuild.__new__(QrBuild)
+            mb.__dict__.update(p=G * self.q, q=self.q, family="TT", keep_trace=True, _h=h, record_updates=False)
+            plan = Plan(mb, self.nb)
+            self._merges[G] = (plan, *plan.alloc(self.dev))
+        return self._merges[G]
+
+    def merge_many(self, rs, key=None):
+        """[R_0; R_1; ...; R_{G-1}] -> merged R (q x q tiles, written into
+        rs[0]), one executor launch (merge_trace(q, G)).  With a key the
+        merge's reflectors and T factors are kept for apply_merge_many."""
+        G, q, t2 = len(rs), self.q, self.nb * self.nb
+        plan, tiles, tg, te = self._merge_setup(G)
+        m = tiles.view(q, G * q * t2)
+        for g, r in enumerate(rs):
+            m[:, g * q * t2:(g + 1) * q * t2].copy_(r.view(q, q * t2))
+        plan.factor(tiles, tg, te)
         if key is not None:
-            self.merge_factors[key] = (self.mtiles.clone(), self.mtg.clone(), self.mte.clone())
-        r_a.view(self.q, self.q * t2).copy_(m[:, :self.q * t2])
-        return r_a
+            self.merge_factors[key] = (G, tiles.clone(), tg.clone(), te.clone())
+        rs[0].view(q, q * t2).copy_(m[:, :q * t2])
+        return rs[0]
+
+    def merge(self, r_a, r_b, key=None):
+        """[R_a; R_b] -> merged R (q x q tiles, written into r_a); see
+        merge_many."""
+        return self.merge_many([r_a, r_b], key)
 
     def apply_local(self, C, trans):
         """Q_local^T C (trans) or Q_local C for this shard's block rows
@@ -263,16 +301,20 @@ class GpuBackend:
         plan.apply_q(trans, self.tiles, self.tg, self.te, ct, cols)
         return plan.unpack(ct, cols)
 
-    def apply_merge(self, key, top_a, top_b, trans):
+    def apply_merge_many(self, key, tops, trans):
         """The merge `key`'s Q^T (trans) or Q applied to the stacked R-rows
-        [top_a; top_b] of C (q*nb x c each); returns the two halves."""
-        plan, h = self.merge_plan, self.q * self.nb
-        cols = top_a.shape[1] // self.nb
-        ct = plan.pack_cols(self.torch.cat([top_a, top_b]), cols)
-        tiles, tg, te = self.merge_factors[key]
+        [tops[0]; tops[1]; ...] of C (q*nb x c each); returns the pieces."""
+        G, tiles, tg, te = self.merge_factors[key]
+        plan, h = self._merge_setup(G)[0], self.q * self.nb
+        cols = tops[0].shape[1] // self.nb
+        ct = plan.pack_cols(self.torch.cat(tops), cols)
         plan.apply_q(trans, tiles, tg, te, ct, cols)
         out = plan.unpack(ct, cols)
-        return out[:h], out[h:]
+        return [out[g * h:(g + 1) * h] for g in range(G)]
+
+    def apply_merge(self, key, top_a, top_b, trans):
+        """Two-block apply_merge_many; returns the two halves."""
+        return tuple(self.apply_merge_many(key, [top_a, top_b], trans))
 
     def r_matrix(self, rbuf):
         """Upper-triangular n x n R from a q x q tile block."""
@@ -288,16 +330,19 @@ def _upper_tiles(q):
     return [j * q + i for j in range(q) for i in range(j + 1)]
 
 
-def tall_skinny_qr(A_local, backend, rank, world, dist=None, keep_q=False):
+def tall_skinny_qr(A_local, backend, rank, world, dist=None, keep_q=False, merge="binary"):
     """Factor the block rows A_local on every rank; rank 0 returns the final
     q x q-tile R block (others return None).  `dist` is torch.distributed
     (send/recv of the R block; NCCL on GPUs, gloo in the CPU tests).  Only
     the q(q+1)/2 tiles of R's upper block triangle travel (18 MiB at q = 8
     instead of 32): the merge trace never reads a tile below the block
-    diagonal.  A_local on the host (page-locked, GpuBackend) streams in while
-    the local factorization runs.  keep_q keeps every merge's factors on the
-    receiving rank for tall_skinny_apply_q (the local factors stay in the
-    backend until its next factorization)."""
+    diagonal.  merge="gather": every rank sends its block to rank 0 at once
+    and rank 0 merges all G in one launch (merge_many: one exchange step and
+    a critical path of ~1.6 binary merges at G = 8 instead of log2 G = 3).
+    A_local on the host (page-locked, GpuBackend) streams in while the local
+    factorization runs.  keep_q keeps every merge's factors on the receiving
+    rank for tall_skinny_apply_q (the local factors stay in the backend
+    until its next factorization)."""
     if getattr(A_local, "is_cuda", True) or not hasattr(backend, "factor_local_host"):
         r = backend.factor_local(A_local)
     else:
@@ -309,6 +354,19 @@ def tall_skinny_qr(A_local, backend, rank, world, dist=None, keep_q=False):
     q = backend.q
     t2 = r.numel() // (q * q)
     up = torch.tensor(_upper_tiles(q), dtype=torch.long, device=r.device)
+    if merge == "gather":
+        if rank != 0:
+            dist.send(r.view(q * q, t2).index_select(0, up), dst=0)
+            return None
+        packed = [r.new_empty((len(up), t2)) for _ in range(world - 1)]
+        reqs = [dist.irecv(packed[g - 1], src=g) for g in range(1, world)]
+        rs = [r]
+        for g in range(1, world):
+            reqs[g - 1].wait()
+            full = r.new_zeros(r.shape)
+            full.view(q * q, t2).index_copy_(0, up, packed[g - 1])
+            rs.append(full)
+        return backend.merge_many(rs, key="gather" if keep_q else None)
     recv = None
     for stride, pairs in rounds:
         for a, b in pairs:
@@ -324,7 +382,7 @@ def tall_skinny_qr(A_local, backend, rank, world, dist=None, keep_q=False):
     return r if rank == 0 else None
 
 
-def tall_skinny_apply_q(C_local, backend, rank, world, trans, dist=None):
+def tall_skinny_apply_q(C_local, backend, rank, world, trans, dist=None, merge="binary"):
     """Q^T C (trans=True) or Q C (trans=False) for the Q of a
     tall_skinny_qr(..., keep_q=True) on the same ranks: C is block-row
     sharded like A (C_local: this rank's P*nb rows, on the backend's device).
@@ -336,6 +394,22 @@ def tall_skinny_apply_q(C_local, backend, rank, world, trans, dist=None):
     h = backend.q * backend.nb
     rounds = merge_rounds(world)
     c = backend.apply_local(C_local, True) if trans else C_local.clone()
+    if merge == "gather" and world > 1:
+        # the stacked R-rows of every rank go to rank 0 and come back
+        if rank != 0:
+            top = c[:h].contiguous()
+            dist.send(top, dst=0)
+            dist.recv(top, src=0)
+            c[:h].copy_(top)
+        else:
+            tops = [c[:h]] + [c[:h].new_empty(c[:h].shape) for _ in range(world - 1)]
+            for g in range(1, world):
+                dist.recv(tops[g], src=g)
+            outs = backend.apply_merge_many("gather", tops, trans)
+            c[:h].copy_(outs[0])
+            for g in range(1, world):
+                dist.send(outs[g].contiguous(), dst=g)
+        rounds = []
     for stride, pairs in (rounds if trans else rounds[::-1]):
         for a, b in pairs:
             if rank == b:

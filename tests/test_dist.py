@@ -29,6 +29,19 @@ def test_composite_list_matches_reference(golden, key):
         assert build_digest(b) == rec["trace_sha"]
 
 
+@pytest.mark.parametrize("p,q,G", [(64, 8, 8), (16, 4, 4), (24, 4, 3), (8192, 8, 8)])
+def test_gather_composite_list_valid(p, q, G):
+    """Local Greedy trees + one gather merge of all G R factors: a valid
+    elimination list under the reference's rules (qr.py:56-83, the C++
+    validator), total weight unchanged (qr.py:663-677)."""
+    lst = dist.composite_list(p, q, G, merge="gather")
+    assert lst.validate()
+    b = P.tiled_build(lst, keep_trace=False)
+    assert b.total_weight == P.total_weight(p, q)
+    kinds, _ = dist.merge_trace(q, G)
+    assert len(kinds) > 0
+
+
 def test_merge_trace_is_the_tail_of_the_global_trace():
     p, q, G = 16, 4, 2
     Pp = p // G
@@ -54,7 +67,6 @@ class CpuOracleBackend:
 
     def __init__(self, Pp, q, nb, device=None):
         self.Pp, self.q, self.nb = Pp, q, nb
-        self.kinds, self.idx = dist.merge_trace(q)
 
     def _block(self, tiles):
         out = torch.empty(self.q * self.q * self.nb * self.nb, dtype=torch.float64)
@@ -76,23 +88,31 @@ class CpuOracleBackend:
         self.merges = {}
         return self._block(rp.t)
 
-    def merge(self, r_a, r_b, key=None):
+    def merge_many(self, rs, key=None):
+        G = len(rs)
+        kinds, idx = dist.merge_trace(self.q, G)
         rp = Replay.__new__(Replay)
-        rp.p, rp.q, rp.nb, rp.ib = 2 * self.q, self.q, self.nb, 32
-        rp.t = self._tiles(r_a) + self._tiles(r_b)
+        rp.p, rp.q, rp.nb, rp.ib = G * self.q, self.q, self.nb, 32
+        rp.t = sum((self._tiles(r) for r in rs), [])
         rp.tg, rp.te = {}, {}
-        rp.run(self.kinds, self.idx)
+        rp.run(kinds, idx)
         if key is not None:
-            self.merges[key] = (rp, self.kinds, self.idx)
+            self.merges[key] = (rp, kinds, idx)
         return self._block(rp.t[:self.q])
+
+    def merge(self, r_a, r_b, key=None):
+        return self.merge_many([r_a, r_b], key)
 
     def apply_local(self, C, trans):
         return torch.from_numpy(_replay_apply(*self.local, C.numpy(), trans))
 
-    def apply_merge(self, key, top_a, top_b, trans):
-        out = _replay_apply(*self.merges[key], np.vstack([top_a.numpy(), top_b.numpy()]), trans)
+    def apply_merge_many(self, key, tops, trans):
+        out = _replay_apply(*self.merges[key], np.vstack([t.numpy() for t in tops]), trans)
         h = self.q * self.nb
-        return torch.from_numpy(out[:h].copy()), torch.from_numpy(out[h:].copy())
+        return [torch.from_numpy(out[g * h:(g + 1) * h].copy()) for g in range(len(tops))]
+
+    def apply_merge(self, key, top_a, top_b, trans):
+        return tuple(self.apply_merge_many(key, [top_a, top_b], trans))
 
 
 def _replay_apply(rp, kinds, idx, C, trans):
@@ -131,7 +151,7 @@ def _matrix(p, q, nb, seed=4):
     return np.random.default_rng(seed).uniform(-1.0, 1.0, (p * nb, q * nb))
 
 
-def _worker(rank, world, port, p, q, nb, out):
+def _worker(rank, world, port, p, q, nb, out, merge="binary"):
     import torch.distributed as td
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -140,13 +160,13 @@ def _worker(rank, world, port, p, q, nb, out):
     Pp = p // world
     A_local = torch.from_numpy(A[rank * Pp * nb:(rank + 1) * Pp * nb].copy())
     be = CpuOracleBackend(Pp, q, nb)
-    r = dist.tall_skinny_qr(A_local, be, rank, world, td, keep_q=True)
+    r = dist.tall_skinny_qr(A_local, be, rank, world, td, keep_q=True, merge=merge)
     # distributed apply-Q: Q^T A = [R; 0] on the block rows, Q [I; 0] = Q
-    qta = dist.tall_skinny_apply_q(A_local.clone(), be, rank, world, True, td)
+    qta = dist.tall_skinny_apply_q(A_local.clone(), be, rank, world, True, td, merge=merge)
     E = np.zeros_like(A)
     E[:q * nb] = np.eye(q * nb)
     ql = dist.tall_skinny_apply_q(torch.from_numpy(E[rank * Pp * nb:(rank + 1) * Pp * nb].copy()), be, rank, world,
-                                  False, td)
+                                  False, td, merge=merge)
     parts = [torch.empty_like(ql) for _ in range(world)]
     td.all_gather(parts, ql)
     tparts = [torch.empty_like(qta) for _ in range(world)]
@@ -164,28 +184,29 @@ def _worker(rank, world, port, p, q, nb, out):
     td.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_gloo_exchange_and_merge(world):
+@pytest.mark.parametrize("world,merge", [(2, "binary"), (4, "binary"), (4, "gather"), (3, "gather")])
+def test_gloo_exchange_and_merge(world, merge):
     import torch.multiprocessing as mp
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    mp.spawn(_worker, args=(world, port, 4 * world, 2, 64, q), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, 4 * world, 2, 64, q, merge), nprocs=world, join=True)
     err_r, res, orth, qta = q.get(timeout=60)
     assert err_r <= 1e-13, err_r
     assert res <= 1e-14 and orth <= 1e-13 and qta <= 1e-14, (res, orth, qta)
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("G,p,q,nb", [(2, 8, 2, 64), (4, 16, 4, 64), (2, 8, 4, 256)])
-def test_gpu_emulated_shards(G, p, q, nb):
+@pytest.mark.parametrize("G,p,q,nb,merge", [(2, 8, 2, 64, "binary"), (4, 16, 4, 64, "binary"), (2, 8, 4, 256, "binary"),
+                                            (4, 16, 4, 64, "gather"), (8, 32, 4, 256, "gather")])
+def test_gpu_emulated_shards(G, p, q, nb, merge):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     A = _matrix(p, q, nb, seed=7)
     At = torch.from_numpy(A).cuda()
-    be, r = dist.emulate(At, G, nb, device=torch.device("cuda"))
+    be, r = dist.emulate(At, G, nb, device=torch.device("cuda"), merge=merge)
     R = row_sign_normalize(be.r_matrix(r).cpu().numpy())
     Rref = row_sign_normalize(np.linalg.qr(A, mode="r"))
     assert np.linalg.norm(R - Rref) <= 1e-11 * np.linalg.norm(A)
@@ -207,21 +228,22 @@ def test_gpu_streamed_local_factorization_matches_device_path():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("G,p,q,nb", [(2, 8, 2, 64), (4, 16, 4, 64), (4, 16, 2, 256)])
-def test_gpu_emulated_apply_q(G, p, q, nb):
+@pytest.mark.parametrize("G,p,q,nb,merge", [(2, 8, 2, 64, "binary"), (4, 16, 4, 64, "binary"), (4, 16, 2, 256, "binary"),
+                                            (4, 16, 4, 64, "gather"), (8, 16, 2, 256, "gather")])
+def test_gpu_emulated_apply_q(G, p, q, nb, merge):
     """Distributed apply-Q on the device (shards emulated on one GPU):
     Q [I; 0] is orthonormal with A = Q R, and Q^T A = [R; 0]."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     A = _matrix(p, q, nb, seed=13)
     At = torch.from_numpy(A).cuda()
-    bes, r = dist.emulate(At, G, nb, device=torch.device("cuda"), keep=True)
+    bes, r = dist.emulate(At, G, nb, device=torch.device("cuda"), keep=True, merge=merge)
     Rf = bes[0].r_matrix(r)
     n = q * nb
     E = torch.zeros_like(At)
     E[:n].fill_diagonal_(1.0)
-    Q = torch.cat(dist.emulate_apply_q(bes, E, False))
-    QtA = torch.cat(dist.emulate_apply_q(bes, At, True))
+    Q = torch.cat(dist.emulate_apply_q(bes, E, False, merge=merge))
+    QtA = torch.cat(dist.emulate_apply_q(bes, At, True, merge=merge))
     nA = torch.linalg.norm(At)
     assert torch.linalg.norm(At - Q @ Rf) / nA <= 1e-12
     assert torch.linalg.norm(Q.T @ Q - torch.eye(n, dtype=torch.float64, device="cuda")) <= 1e-12

@@ -273,6 +273,25 @@ class TiledQR:
         return self.apply_q(E, trans=False)
 
 
+_PLAN_CACHE = {}
+_PLAN_CACHE_MAX = 8
+
+
+def cached_plan(p, q, nb, ib=32, algo="greedy", family="TT", bs=None, grasap_i=1, io=0):
+    """Compiled Plan for a tree on p x q tiles, kept in a small per-process
+    cache (least recently used out): repeated tiled_qr calls on one shape
+    pay the schedule compile (build_tree + tqr_plan_create) once.  Plans
+    are immutable and safe to share (per-launch scratch)."""
+    key = (p, q, nb, ib, algo.lower(), family, bs, grasap_i, io, torch.cuda.current_device())
+    plan = _PLAN_CACHE.pop(key, None)
+    if plan is None:
+        plan = Plan(build_tree(p, q, algo, family=family, bs=bs, grasap_i=grasap_i), nb, ib, io=io)
+    _PLAN_CACHE[key] = plan
+    while len(_PLAN_CACHE) > _PLAN_CACHE_MAX:
+        _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
+    return plan
+
+
 def tiled_qr_host(A_host, R_host=None, nb=256, algo="greedy", family="TT", bs=None, grasap_i=1, plan=None,
                   buffers=None):
     """Host matrix in, host R out, with the transfers overlapped with the
@@ -291,8 +310,7 @@ def tiled_qr_host(A_host, R_host=None, nb=256, algo="greedy", family="TT", bs=No
     elif not (A_host.is_pinned() and A_host.stride(1) == 1 and A_host.stride(0) >= A_host.shape[1]):
         A_host = A_host.contiguous().pin_memory()  # row-major, unit column stride
     if plan is None:
-        build = build_tree(p, q, algo, family=family, bs=bs, grasap_i=grasap_i)
-        plan = Plan(build, nb, io=Plan.IO_IN | Plan.IO_OUT)
+        plan = cached_plan(p, q, nb, algo=algo, family=family, bs=bs, grasap_i=grasap_i, io=Plan.IO_IN | Plan.IO_OUT)
     R_pad = R_host if (R_host is not None and shape[1] == q * nb) else None
     if R_pad is None:
         R_pad = torch.zeros((q * nb, q * nb), dtype=torch.float64).pin_memory()
@@ -339,9 +357,9 @@ def tiled_qr(A, nb=256, ib=32, algo="greedy", family="TT", bs=None, grasap_i=1, 
             if (elim.p, elim.q) != (p, q):
                 raise ValueError(f"list is for {elim.p}x{elim.q} tiles, matrix has {p}x{q}")
             build = tiled_build(elim, family)
+            plan = Plan(build, nb, ib)
         else:
-            build = build_tree(p, q, algo, family=family, bs=bs, grasap_i=grasap_i)
-        plan = Plan(build, nb, ib)
+            plan = cached_plan(p, q, nb, ib, algo=algo, family=family, bs=bs, grasap_i=grasap_i)
     if not A.is_cuda:
         A = A.cuda()
     tiles, tg, te = plan.alloc(A.device)

@@ -521,3 +521,18 @@ def test_asap_grasap_at_scale(algo, p, q, nb):
         n = R.shape[0]
         assert torch.linalg.norm(QtA[:n] - R).item() / nA <= 1e-12
         assert torch.linalg.norm(QtA[n:]).item() / nA <= 1e-12
+
+
+def test_cli_numeric_gantt(tmp_path):
+    """qr-numeric --check --gantt: the device timeline in the reference's
+    Gantt CSV layout (sched.py:45-49), one row per work item."""
+    _need_gpu()
+    from paper_1303_3182_b200.cli import main
+    g = tmp_path / "g.csv"
+    assert main(["qr-numeric", "--p", "6", "--q", "3", "--nb", "64", "--check", "--gantt", str(g)]) == 0
+    lines = g.read_text().splitlines()
+    assert lines[0] == "proc,start,end,kind,i,j,k"
+    plan = Plan(P.build_tree(6, 3, "greedy"), 64)
+    assert len(lines) - 1 == plan.info.n_items
+    kinds = {ln.split(",")[3] for ln in lines[1:]}
+    assert {"GEQRT", "TTQRT", "UNMQR", "TTMQR"} <= kinds

@@ -324,17 +324,19 @@ def run_single(args, name, cfg):
         bufs = plan_io.stream_buffers()
         tiled_qr_host(A_pin, R_pin, plan=plan_io, buffers=bufs)  # warm-up
         torch.cuda.synchronize()
-        ne = max(1, min(args.steps, 3))
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(ne):
+        ne = max(3, min(args.steps, 5))
+        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ne)]
+        for a, b in eev:
+            a.record()
             tiled_qr_host(A_pin, R_pin, plan=plan_io, buffers=bufs)
-        e1.record()
+            b.record()
         torch.cuda.synchronize()
-        e_ms = e0.elapsed_time(e1) / ne
+        each = [a.elapsed_time(b) for a, b in eev]
+        e_ms = statistics.mean(each)
         ok = ok and bool(torch.equal(R_pin, R.cpu()))  # same R as the device-resident path
         e2e = {"value": round(flops / (e_ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
-               "ms_per_step": round(e_ms, 3), "api": "tiled_qr_host (pinned host A in, pinned host R out)",
+               "ms_per_step": round(e_ms, 3), "ms_each": [round(x, 2) for x in each],
+               "api": "tiled_qr_host (pinned host A in, pinned host R out)",
                "cold_call_ms": round(cold_ms, 1),
                "cold_call": "first tiled_qr_host call on the shape: + schedule compile, scratch allocation (wall)",
                "h2d_bytes_per_step": int(A_host.nbytes),

@@ -57,8 +57,11 @@ class Plan:
 
     def __del__(self):
         h = self.__dict__.get("_h")
-        if h is not None and _lib._lib is not None:
-            _lib._lib.tqr_plan_free(h)
+        try:
+            if h is not None and _lib._lib is not None:
+                _lib._lib.tqr_plan_free(h)
+        except (AttributeError, TypeError):  # interpreter shutdown: modules already torn down
+            pass
 
     def alloc(self, device=None):
         dev = device or torch.device("cuda", torch.cuda.current_device())

@@ -315,8 +315,11 @@ class QrBuild:
 
     def __del__(self):
         h = self.__dict__.get("_h")
-        if h is not None and _lib._lib is not None:
-            _lib._lib.tqr_build_free(h)
+        try:
+            if h is not None and _lib._lib is not None:
+                _lib._lib.tqr_build_free(h)
+        except (AttributeError, TypeError):  # interpreter shutdown: modules already torn down
+            pass
 
     def trace_arrays(self):
         """(kind int8[n], idx int32[n,4], finish int64[n]) of the trace."""

@@ -135,6 +135,11 @@ struct DevSched {
   int32_t* preds = nullptr;
   int n_items = 0;
   int64_t n_preds = 0;
+  // look-ahead dequeue (each CTA holds its next item while running the
+  // current one: the next update's first reflector block is staged early).
+  // Off for critical-path-bound schedules, where a held panel waits behind
+  // a long item (C4: 27.2 -> 23.6 ms without; C3: 259.5 -> 268.1 ms).
+  bool lookahead = true;
   std::shared_ptr<ScratchPool> scratch = std::make_shared<ScratchPool>();
   void free_all() {
     cudaFree(items);
@@ -228,10 +233,13 @@ inline double item_cost(int kind, int nb, double panel) {
 // taskgraph.py:338-362) and lowest-id tie break, the MaxCP policy of the
 // reference's list scheduler (sched.py:77-156).  The result is a
 // topological order, which the executor's deadlock-freedom needs.
-void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers, int nb,
+// Returns whether the simulated schedule is throughput-bound (makespan within
+// 1.25x of the total work over the workers) rather than critical-path-bound;
+// the executor's dequeue policy follows it.
+bool cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers, int nb,
               const std::vector<double>& unit_release = {}, int acr = 1, int anch = 1) {
   const size_t n = items.size();
-  if (n == 0) return;
+  if (n == 0) return true;
   std::vector<int32_t> nsucc(n + 1, 0);
   for (size_t v = 0; v < n; ++v)
     for (int32_t k = 0; k < items[v].pred_n; ++k) nsucc[size_t(preds[size_t(items[v].pred_lo + k)]) + 1]++;
@@ -252,7 +260,8 @@ void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers
   // tools/cost_sweep.sh)
   size_t n_upd = 0;
   for (size_t v = 0; v < n; ++v) n_upd += (items[v].kind >= tqr::UNMQR && items[v].kind <= tqr::TSMQR);
-  const double panel = env_cost("TQR_COST_PANEL", n_upd >= 2000 * size_t(workers) ? 3.0 : 8.0);
+  const bool throughput = n_upd >= 2000 * size_t(workers);
+  const double panel = env_cost("TQR_COST_PANEL", throughput ? 3.0 : 8.0);
   for (size_t v = 0; v < n; ++v) w[v] = item_cost(items[v].kind, nb, panel);
   // simulated durations: the panel cost may differ from the one the
   // priorities use (TQR_SIM_PANEL: panel items' duration multiplier)
@@ -321,6 +330,13 @@ void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers
     }
   }
   if (order.size() != n) throw std::runtime_error("cp_order: dependency cycle");
+  double work = 0.0, makespan = now;
+  for (size_t v = 0; v < n; ++v) work += wd[v];
+  while (!running.empty()) {
+    makespan = std::max(makespan, running.top().first);
+    running.pop();
+  }
+  const bool throughput_bound = makespan <= 1.25 * work / double(std::max(workers, 1));
   std::vector<int32_t> pos(n);
   for (size_t t = 0; t < n; ++t) pos[size_t(order[t])] = int32_t(t);
   std::vector<Item> ni(n);
@@ -335,6 +351,8 @@ void cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers
   }
   items.swap(ni);
   preds.swap(np);
+  (void)throughput;
+  return throughput_bound;
 }
 
 void upload(DevSched& d, const std::vector<Item>& items, const std::vector<int32_t>& preds) {
@@ -440,7 +458,8 @@ cudaError_t run(const DevSched& d, int nb, bool apply, bool transT, const double
     if ((e = cudaMemsetAsync(sl->queue, 0, sizeof(int), st)) != cudaSuccess) return e;
   }
   DevView v{d.items, d.preds, sl->done, sl->queue, d.n_items};
-  tqrx::g_flags = env_int("TQR_FLAGS", 0);
+  // TQR_FLAGS overrides the plan's choice entirely (debug / A-B runs)
+  tqrx::g_flags = env_int("TQR_FLAGS", d.lookahead ? 0 : 4);
   tqrx::g_carveout = env_int("TQR_CARVEOUT", -1);
   const int grid = std::min(d.n_items, std::max(1, env_int("TQR_GRID", num_sms())));
   // factorization: <nb, true, false>; apply-Q: <nb, trans, true> (compensated)
@@ -568,8 +587,9 @@ int tqr_plan_create_io(const tqr_build* hb, int nb, int ib, int io, tqr_plan** o
       std::vector<Item> items;
       std::vector<int32_t> preds;
       expand(tasks, in, order, nb / WS, items, preds);
-      cp_order(items, preds, num_sms_host(), nb, unit_release, P->acr, P->anch);
+      const bool thr = cp_order(items, preds, num_sms_host(), nb, unit_release, P->acr, P->anch);
       upload(P->fac, items, preds);
+      P->fac.lookahead = thr;
       const double mm = double(b.p) * nb, nn = double(b.q) * nb;
       P->flops = 2.0 * nn * nn * (mm - nn / 3.0);
     } catch (...) {
@@ -782,9 +802,10 @@ int tqr_apply_q(tqr_plan* P, int trans, const double* tiles, const double* tg, c
     std::vector<Item> items;
     std::vector<int32_t> preds;
     expand(tasks, in, order, P->nb / WS, items, preds);
-    cp_order(items, preds, num_sms_host(), P->nb);
+    const bool thr = cp_order(items, preds, num_sms_host(), P->nb);
     DevSched d;
     upload(d, items, preds);
+    d.lookahead = thr;
     P->aq[key] = d;
   });
   if (rc) return rc;

@@ -194,7 +194,9 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
     mbar_init(&bars[2], NW);
     mbar_init(&bars[3], NW);
     s_cur = atomicAdd(P.queue, 1);
-    s_nxt = s_cur < P.n_items ? atomicAdd(P.queue, 1) : P.n_items;
+    // flags bit 2: no look-ahead dequeue (an item is taken only when the CTA
+    // is free: no early staging, but no item held behind a long one either)
+    s_nxt = (s_cur < P.n_items && !(P.flags & 4)) ? atomicAdd(P.queue, 1) : P.n_items;
     s_ready = -1;
   }
   bar_all();
@@ -345,8 +347,13 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
         P.trace[4 * size_t(it) + 2] = gtimer();
         P.trace[4 * size_t(it) + 3] = smid();
       }
-      s_cur = nx;
-      s_nxt = nx < P.n_items ? atomicAdd(P.queue, 1) : P.n_items;
+      if (P.flags & 4) {
+        s_cur = atomicAdd(P.queue, 1);
+        s_nxt = P.n_items;
+      } else {
+        s_cur = nx;
+        s_nxt = nx < P.n_items ? atomicAdd(P.queue, 1) : P.n_items;
+      }
     }
     bar_all();
     it = s_cur;

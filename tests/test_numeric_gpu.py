@@ -256,13 +256,13 @@ def test_arrival_units_cover_tiles_column_major():
 def test_executor_schedule_independent_and_deterministic(p, q, nb, monkeypatch):
     """The per-tile kernel sequence is fixed by the hazard DAG, so the factored
     tiles are bit-identical for any number of CTAs, with or without early
-    staging / L2 prefetch, and across repeated runs (a race in the dependency
+    staging / L2 prefetch / look-ahead dequeue, and across repeated runs (a race in the dependency
     protocol would show up as a difference)."""
     _need_gpu()
     A = torch.from_numpy(np.random.default_rng(31).standard_normal((p * nb, q * nb))).cuda()
     plan = Plan(P.build_tree(p, q, "greedy"), nb)
     ref = None
-    for grid, flags in [(148, 0), (1, 0), (7, 0), (37, 1), (148, 2), (148, 3)] + [(148, 0)] * 8:
+    for grid, flags in [(148, 0), (1, 0), (7, 0), (37, 1), (148, 2), (148, 3), (148, 4), (5, 4)] + [(148, 0)] * 8:
         monkeypatch.setenv("TQR_GRID", str(grid))
         monkeypatch.setenv("TQR_FLAGS", str(flags))
         tiles, tg, te = plan.alloc()

@@ -564,11 +564,14 @@ int tqr_plan_create_io(const tqr_build* hb, int nb, int ib, int io, tqr_plan** o
         // modeled arrival (item-cost units, ~50 GB/s host link; an update
         // slab item ~ 54 us at nb=256), indexed by flag (j-1)*anch + c
         const double unit_s = 54e-6 * (double(nb) / 256.0) * (double(nb) / 256.0);
+        // modeled pinned H2D rate (measured ~47.7 GB/s on the pool's boxes);
+        // TQR_H2D_GBS overrides
+        static const double h2d_bps = env_cost("TQR_H2D_GBS", 48.0) * 1e9;
         unit_release.assign(size_t(b.q) * P->anch, 0.0);
         double t = 0.0;
         for (size_t u = 0; u < P->arrival.size() / 3; ++u) {
           const int j = P->arrival[3 * u], c = (P->arrival[3 * u + 1] - 1) / P->acr;
-          t += double(P->arrival[3 * u + 2]) * nb * nb * 8.0 / 50e9 / unit_s;
+          t += double(P->arrival[3 * u + 2]) * nb * nb * 8.0 / h2d_bps / unit_s;
           unit_release[size_t(j - 1) * P->anch + c] = t;
         }
       }

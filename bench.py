@@ -400,7 +400,9 @@ def run_c5(args, name, cfg):
         """(ms per step, R block on rank 0, backend) for G shards."""
         P = p // G
         A = torch.from_numpy(A_host).to(dev)
+        t_p = time.perf_counter()
         be = dist.GpuBackend(P, q, nb, dev, algo=cfg["algo"])
+        plan_times[G] = round(time.perf_counter() - t_p, 3)
 
         def step():
             return dist.tall_skinny_qr(A, be, rank_, G, comm, merge=args.merge)
@@ -422,6 +424,7 @@ def run_c5(args, name, cfg):
         del A
         return ms, out, be
 
+    plan_times = {}
     single = None
     if world > 1 and rank == 0 and not args.no_single:
         # rank 0's same-run one-GPU C5 (the N=1 point of this scaling line);
@@ -509,6 +512,7 @@ def run_c5(args, name, cfg):
                          "kernel": "exec_kernel (local factorization + merges)",
                          "peak_source": "live DMMA.8x8x4 probe x n_gpus"},
             "clocks": clocks, "cpu_baseline": cpu, "e2e": e2e, "nccl": nccl,
+            "plan_s": plan_times.get(world),
             "check": {"r_finite": ok},
         }
         if single is not None:

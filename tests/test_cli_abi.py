@@ -83,3 +83,34 @@ def test_cli_check_compares_every_cell(monkeypatch, capsys, cmd, kind, key):
     monkeypatch.setattr(cli, "_golden_cells", lambda k, kk: bad)
     assert main(cmd.split()) == 1
     assert "(4,2)" in capsys.readouterr().err
+
+
+def _build_c_example(tmp_path):
+    """Compile tests/c_host/example.c (a plain C host of include/tqr.h) with
+    gcc against the in-tree libtqr.so; None if no C compiler."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        return None
+    lib_dir = os.path.join(ROOT, "paper_1303_3182_b200")
+    exe = str(tmp_path / "tqr_example")
+    cmd = [cc, "-O2", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "c_host", "example.c"), "-L", lib_dir, "-ltqr",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", "-lm", f"-Wl,-rpath,{lib_dir}",
+           "-Wl,-rpath,/usr/local/cuda/lib64", "-o", exe]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_host_schedule(tmp_path):
+    """The C ABI from a C program (no Python): build_tree golden cp/weight and
+    the reference's error message, without a GPU."""
+    import subprocess
+    exe = _build_c_example(tmp_path)
+    if exe is None:
+        pytest.skip("no C compiler")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "cp 78, total weight 640" in r.stdout and "need p >= q >= 1" in r.stdout

@@ -536,3 +536,17 @@ def test_cli_numeric_gantt(tmp_path):
     assert len(lines) - 1 == plan.info.n_items
     kinds = {ln.split(",")[3] for ln in lines[1:]}
     assert {"GEQRT", "TTQRT", "UNMQR", "TTMQR"} <= kinds
+
+
+def test_c_host_factorization(tmp_path):
+    """A plain C host of include/tqr.h (tests/c_host/example.c): plan,
+    pack, factor, extract R on the device through the C ABI only."""
+    _need_gpu()
+    import subprocess
+    from test_cli_abi import _build_c_example
+    exe = _build_c_example(tmp_path)
+    if exe is None:
+        pytest.skip("no C compiler")
+    r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "gpu ok" in r.stdout and "nb = 100 rejected" in r.stdout

@@ -340,20 +340,55 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
     // take the item after next now; the producer warpgroup publishes `it`
     // after the barrier (its fence waits for this CTA's stores to drain while
     // the consumers already start the next item)
-    if (tid == 0) {
-      if (P.trace) {
-        P.trace[4 * size_t(it)] = t_deq;
-        P.trace[4 * size_t(it) + 1] = t_rdy;
-        P.trace[4 * size_t(it) + 2] = gtimer();
-        P.trace[4 * size_t(it) + 3] = smid();
-      }
-      if (P.flags & 4) {
+    if (tid == 0 && P.trace) {
+      P.trace[4 * size_t(it)] = t_deq;
+      P.trace[4 * size_t(it) + 1] = t_rdy;
+      P.trace[4 * size_t(it) + 2] = gtimer();
+      P.trace[4 * size_t(it) + 3] = smid();
+    }
+    if (P.flags & 4) {
+      if (tid == 0) {
         s_cur = atomicAdd(P.queue, 1);
         s_nxt = P.n_items;
-      } else {
-        s_cur = nx;
-        s_nxt = nx < P.n_items ? atomicAdd(P.queue, 1) : P.n_items;
       }
+    } else if (!(P.flags & 8) && nx < P.n_items && s_ready != nx) {
+      // opportunistic order: the held item nx was not found ready by the
+      // producer; if it still is not, take the next item from the queue and,
+      // when that one is ready, run it first (nx stays held).  Deadlock-free:
+      // a CTA only ever waits on the earliest item it holds, and the globally
+      // earliest unfinished item is always ready.  Predecessors equal to the
+      // item just finished count as done (published right after the barrier).
+      if (warp == 0) {
+        auto ready = [&](int x) {
+          const Item X = P.items[x];
+          int ok = 1;
+          for (int t = lane; t < X.pred_n; t += 32) {
+            const int pr = P.preds[X.pred_lo + t];
+            if (pr != it && ld_acquire(P.done + pr) == 0) ok = 0;
+          }
+          return __all_sync(0xffffffffu, ok) != 0;
+        };
+        int cur = nx, nxt;
+        if (ready(nx)) {
+          nxt = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(P.queue, 1) : 0, 0);
+        } else {
+          const int c = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(P.queue, 1) : 0, 0);
+          if (c < P.n_items && ready(c)) {
+            cur = c;
+            nxt = nx;
+          } else {
+            nxt = c;
+          }
+          if (P.trace && lane == 0) atomicAdd(P.trace + 4 * size_t(P.n_items) + 58 + (cur == c ? 0 : 1), 1ull);
+        }
+        if (lane == 0) {
+          s_cur = cur;
+          s_nxt = nxt;
+        }
+      }
+    } else if (tid == 0) {
+      s_cur = nx;
+      s_nxt = nx < P.n_items ? atomicAdd(P.queue, 1) : P.n_items;
     }
     bar_all();
     it = s_cur;

@@ -262,7 +262,8 @@ def test_executor_schedule_independent_and_deterministic(p, q, nb, monkeypatch):
     A = torch.from_numpy(np.random.default_rng(31).standard_normal((p * nb, q * nb))).cuda()
     plan = Plan(P.build_tree(p, q, "greedy"), nb)
     ref = None
-    for grid, flags in [(148, 0), (1, 0), (7, 0), (37, 1), (148, 2), (148, 3), (148, 4), (5, 4)] + [(148, 0)] * 8:
+    for grid, flags in [(148, 0), (1, 0), (7, 0), (37, 1), (148, 2), (148, 3), (148, 4), (5, 4), (148, 8),
+                        (3, 0)] + [(148, 0)] * 8:
         monkeypatch.setenv("TQR_GRID", str(grid))
         monkeypatch.setenv("TQR_FLAGS", str(flags))
         tiles, tg, te = plan.alloc()

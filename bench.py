@@ -597,6 +597,8 @@ def parse_args(argv=None):
     ap.add_argument("--ref-step-s", type=float, default=3.0, help="CPU replay window per step (s)")
     ap.add_argument("--dry", action="store_true", help="CPU launcher check: ranks, gloo exchange, no kernels")
     ap.add_argument("--tree", default=None, help="override the workload's elimination tree (e.g. asap, grasap)")
+    ap.add_argument("--family", default=None, choices=["TT", "TS"],
+                    help="override the workload's kernel family (tiledag family= of tiled_build/build_tree)")
     ap.add_argument("--merge", default="gather", choices=["gather", "binary"],
                     help="C5 R merges: one gather merge on rank 0, or log2 N binary rounds")
     args = ap.parse_args(argv)
@@ -612,6 +614,8 @@ def main():
     name, cfg = args.config, CONFIGS[args.config]
     if args.tree:
         cfg = dict(cfg, algo=args.tree)
+    if args.family:
+        cfg = dict(cfg, family=args.family)
     if args.impl == "reference":
         return run_reference(args, name, cfg)
     if args.dry:

@@ -36,12 +36,21 @@ __device__ unsigned long long g_uprof[32];
   } while (0)
 #define UPROF_DECL long long _tp = clock64()
 #define UPROF_DECL_V(v) long long v = clock64()
+// mark once `val` has been produced (a predicate read stalls on its scoreboard)
+#define UPROF_MARK_DEP(k, v, val)                                                                   \
+  do {                                                                                              \
+    asm volatile("{.reg .pred p; setp.eq.f64 p, %0, 0d7FF8000000000123; @p trap;}" ::"d"(val) : "memory"); \
+    UPROF_MARK_V(k, v);                                                                             \
+  } while (0)
 #else
 #define UPROF_MARK(k) \
   do {                \
   } while (0)
 #define UPROF_MARK_V(k, v) \
   do {                     \
+  } while (0)
+#define UPROF_MARK_DEP(k, v, val) \
+  do {                            \
   } while (0)
 #define UPROF_DECL
 #define UPROF_DECL_V(v)
@@ -179,7 +188,11 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
                                              const double* __restrict__ Ts, double* top, int lane,
                                              const double* top_s, int drb, PF& pf, MID& mid) {
   // is V sub-block (row group gg, column group cb) of the diagonal block zero?
+#ifdef TQR_ABL_NODIAG  // ablation: the diagonal block as a full block (V is staged masked)
+  auto zero_blk = [](int, int) { return false; };
+#else
   auto zero_blk = [](int gg, int cb) { return TRI == 0 ? (gg < cb) : (TRI == 1 ? (gg > cb) : false); };
+#endif
   const int r = lane >> 2, c = lane & 3;
   const int s1a = swz_in(2 * c, r);  // (2c+h, r) at s1a + h
   const int s3a = swz_in(r, 2 * c), s3b = swz_in(r, 2 * c + 1);  // (r, 2c+h)
@@ -266,6 +279,8 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
     }
     if (rb == NB / IB / 2 - 1) mid(x);  // (a no-op after its first call)
   }
+  UPROF_MARK_V(10, _tq);
+  UPROF_MARK_DEP(13, _tq, w[KB - 1][1] + w2[KB - 1][1]);
   if constexpr (COMP) {
     // W = top + V^T X summed in double-double, rounded once
 #pragma unroll
@@ -334,10 +349,14 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
 #pragma unroll
       for (int nb = KA; nb < KB; ++nb)
         if (TRANST ? (kb <= nb) : (kb >= nb)) {
+#ifdef TQR_ABL_NOT  // ablation (wrong numbers): no T multiply
+          if (kb == nb) wt[nb][h] = w[kb][h] * tb[h][kb][nb];
+#else
           if constexpr (COMP)
             dmma_comp(wt[nb], wtl[nb], w[kb][h], tb[h][kb][nb]);
           else
             dmma(wt[nb], w[kb][h], tb[h][kb][nb]);
+#endif
         }
   if constexpr (COMP) {
 #pragma unroll
@@ -355,7 +374,8 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
     wt[nb][0] = -wt[nb][0];
     wt[nb][1] = -wt[nb][1];
   }
-  UPROF_MARK_V(11, _tq);
+  UPROF_MARK_V(14, _tq);
+  UPROF_MARK_DEP(11, _tq, wt[KB - 1][1]);
   // X -= W^T V^T ; per 32-row block the product is accumulated from zero and
   // subtracted from X once (LAPACK-like rounding of the large operand)
 #pragma unroll
@@ -408,7 +428,8 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
       }
     }
   }
-  UPROF_MARK_V(12, _tq);
+  UPROF_MARK_V(15, _tq);
+  UPROF_MARK_DEP(12, _tq, x[NB / 8 - 1][0] + x[0][0]);
 }
 
 // Apply the staged ib-block reflector (see warp_apply_k).  SPLIT (off: measured

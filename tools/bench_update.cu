@@ -91,8 +91,13 @@ void run(const char* name, int sms) {
   cudaMemcpyToSymbol(g_uprof, zero, sizeof(zero));
   for (int i = 16; i < 32; ++i) hp[0] += hp[i];
   double tot = double(hp[0] + hp[2] + hp[6] + hp[8]);
-  printf("phases (frac): load_x %.3f wait_full %.3f apply %.3f [gemm1 %.3f T %.3f gemm3 %.3f] store %.3f\n",
-         hp[8] / tot, hp[0] / tot, hp[2] / tot, hp[10] / tot, hp[11] / tot, hp[12] / tot, hp[6] / tot);
+  printf("phases (frac): load_x %.3f wait_full %.3f apply %.3f store %.3f\n", hp[8] / tot, hp[0] / tot, hp[2] / tot,
+         hp[6] / tot);
+  {
+    const double nbw = 8.0 * sms * (reps + 4) * (NB / IB);  // warp-blocks
+    printf("cycles per warp-block: gemm1 issue %.0f drain %.0f | combine+T issue %.0f drain %.0f | gemm2 issue %.0f drain %.0f | total apply %.0f\n",
+           hp[10] / nbw, hp[13] / nbw, hp[14] / nbw, hp[11] / nbw, hp[15] / nbw, hp[12] / nbw, hp[2] / nbw);
+  }
   printf("producer per warp-item: wait empty %.0f issue %.0f\n", hp[3] / (4.0 * 148 * 68), hp[4] / (4.0 * 148 * 68));
   printf("wait_full per block:");
   for (int i = 0; i < 8; ++i) printf(" %.0f", (hp[16 + i] + hp[24 + i]) / (8.0 * 148 * 68));

@@ -27,8 +27,11 @@ def main():
     ap.add_argument("--out", default="gpurun_out/item_trace.json")
     ap.add_argument("--gantt", default=None)
     ap.add_argument("--stream", action="store_true", help="trace the streaming host-to-host path")
+    ap.add_argument("--family", default=None, choices=["TT", "TS"])
     a = ap.parse_args()
     cfg = bench.CONFIGS[a.config]
+    if a.family:
+        cfg = dict(cfg, family=a.family)
     nb = cfg["nb"]
     p, q = cfg["m"] // nb, cfg["n"] // nb
     b = P.build_tree(p, q, cfg["algo"], family=cfg["family"])

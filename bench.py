@@ -401,7 +401,7 @@ def run_c5(args, name, cfg):
         P = p // G
         A = torch.from_numpy(A_host).to(dev)
         t_p = time.perf_counter()
-        be = dist.GpuBackend(P, q, nb, dev, algo=cfg["algo"])
+        be = dist.GpuBackend(P, q, nb, dev, algo=cfg["algo"], family=cfg["family"])
         plan_times[G] = round(time.perf_counter() - t_p, 3)
 
         def step():

@@ -305,16 +305,16 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
     switch (I.kind) {
       case tqr::GEQRT:
         if constexpr (TRANST && !COMP)
-          panel_item<NB, GE>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), nullptr, P.tg + soff<NB>(P.p, I.i, I.k), tid, pprof);
+          panel_run<NB, GE>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), nullptr, P.tg + soff<NB>(P.p, I.i, I.k), tid, pprof);
         break;
       case tqr::TTQRT:
         if constexpr (TRANST && !COMP)
-          panel_item<NB, TT>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.k),
+          panel_run<NB, TT>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.k),
                              P.te + soff<NB>(P.p, I.i, I.k), tid, pprof);
         break;
       case tqr::TSQRT:
         if constexpr (TRANST && !COMP)
-          panel_item<NB, TS>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.k),
+          panel_run<NB, TS>(sm, P.tiles + toff<NB>(P.p, I.i, I.k), P.tiles + toff<NB>(P.p, I.piv, I.k),
                              P.te + soff<NB>(P.p, I.i, I.k), tid, pprof);
         break;
       case tqr::PACK:

@@ -32,7 +32,22 @@ struct Smem {
   static constexpr int P_PART = P_TG + 64, P_DROW = P_PART + 2 * NW * 8, P_SBUF = P_DROW + 16, P_SC = P_SBUF + 8;
   static constexpr int P_SCR_END = P_SC + 3 * IB + 8;
   static constexpr int P_END = (P_V + VS > P_SCR_END) ? P_V + VS : P_SCR_END;
-  static constexpr int END = U_END > P_END ? U_END : P_END;
+  // look-ahead panel (panel_item_la): the staged V of the trailing update
+  // is live while the next block is factored, so only the Gram / T scratch
+  // (G, T plain, the Gram halves' overflow) aliases it; the per-warp partial
+  // W is sized for the FW factorization warps
+  static constexpr int FW = 4;
+  static constexpr int L_W = P_T + TS, L_TG = L_W + 8 * LDW, L_PART = L_TG + 64, L_DROW = L_PART + 2 * NW * 8;
+  static constexpr int L_SBUF = L_DROW + 16, L_SC = L_SBUF + 8, L_WP = L_SC + 3 * IB + 8;
+  static constexpr int L_V = L_WP + FW * 8 * LDW, L_G = L_V + 256, L_TT = L_G + TS;
+  static constexpr int L_END = (L_V + VS > L_TT + TS) ? L_V + VS : L_TT + TS;
+  static_assert(L_V % 2 == 0, "16-byte aligned staging");
+  static constexpr int END0 = U_END > P_END ? U_END : P_END;
+#ifndef TQR_PANEL_NO_LA
+  static constexpr int END = END0 > L_END ? END0 : L_END;
+#else
+  static constexpr int END = END0;
+#endif
   static constexpr size_t BYTES = size_t(END) * sizeof(double);
 };
 
@@ -309,7 +324,8 @@ __device__ __forceinline__ void tn_acc(double (&acc)[NBK][2], const double* P, i
 // row they hold (the next block's write-back stores them).
 template <int NB, int MODE>
 __device__ __noinline__ void panel_trailing(double* at, double* rt, const double* Vs, const double* Ts, int b, int warp,
-                                            int lane, double* P) {
+                                            int lane, double* P, int ch_begin = -1, int ch_end = 1 << 30,
+                                            int ch_step = NW) {
   constexpr int PLD = Smem<NB>::PLD;
   const int rb0 = b * IB;
   const int nch = (NB - rb0 - IB) / 8;
@@ -319,7 +335,9 @@ __device__ __noinline__ void panel_trailing(double* at, double* rt, const double
   // the rows of the lower half load while the first GEMM runs on the upper
   // half (own scoreboard: see update_consume) when the block spans both
   const bool split = g0 < GH && g1 > GH;
-  for (int ch = warp; ch < nch; ch += NW) {
+  // (default: chunk ch on warp ch mod NW; the look-ahead panel gives each
+  // warp group its own chunk range)
+  for (int ch = ch_begin < 0 ? warp : ch_begin; ch < min(nch, ch_end); ch += ch_step) {
     const int col = rb0 + IB + ch * 8;
     double* const xc = at + size_t(col) * NB;
     double x[NB / 8][2];
@@ -903,6 +921,574 @@ __device__ void panel_item(double* sm, double* at /*GE: tile; TT/TS: bottom tile
     csync();
     mark(4);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Look-ahead panel item: the same factorization as panel_item, with the
+// compute warps split in two groups once block 0 is factored.  Warps 0..3
+// (FG) apply block b-1's reflectors to the 32 columns of block b (forwarded
+// into the stacked panel), then run block b's level-2 sweep and group
+// updates (128 threads, up to three panel rows per thread) while warps 4..7
+// (UG) apply block b-1 to the columns right of block b.  Both groups meet
+// for the block Gram, T_b, the write-back and the staging of V_b (all eight
+// warps, as in panel_item).  The level-2 chain is latency-bound and leaves the
+// DMMA pipe idle, the trailing update is DMMA-bound: they overlap instead of
+// adding up.
+template <int NB, int MODE>
+__device__ void panel_item_la(double* sm, double* at /*GE: tile; TT/TS: bottom tile (i,k)*/,
+                              double* rt /*TT/TS: pivot tile (piv,k)*/, double* tslot, int tid,
+                              unsigned long long* prof = nullptr) {
+  using S = Smem<NB>;
+  constexpr int PLD = S::PLD, LDW = S::LDW, FW = S::FW, FT = FW * 32;
+  const int warp = tid >> 5, lane = tid & 31;
+  double* P = sm + S::P_P;
+  double* Ts = sm + S::P_T;
+  double* W = sm + S::L_W;    // [8][LDW]
+  double* Tg = sm + S::L_TG;  // 8x8 group T, Tg[i + j*8]
+  double* part = sm + S::L_PART;
+  double* drow = sm + S::L_DROW;
+  double* sbuf = sm + S::L_SBUF;
+  double* tau_s = sm + S::L_SC;
+  double* taut_s = tau_s + IB;
+  double* beta_s = tau_s + 2 * IB;
+  double* WP = sm + S::L_WP;  // [FW][8][LDW] partial W; Gram halves / T scratch (runs into Vs, dead then)
+  double* Vs = sm + S::L_V;
+  double* G = sm + S::L_G;    // G[l + j*IB] = v_l . v_j   (aliases Vs)
+  double* Tp = sm + S::L_TT;  // T_b plain, row-major      (aliases Vs)
+  const int t = tid;
+  const bool fg = warp < FW;
+  auto fsync = [&]() { asm volatile("bar.sync 3, %0;\n" ::"n"(FT) : "memory"); };
+  unsigned long long tp = (prof && tid == 0) ? ptimer() : 0;
+  auto mark = [&](int ph) {
+    if (prof && tid == 0) {
+      const unsigned long long t2 = ptimer();
+      atomicAdd(prof + MODE * 16 + ph, t2 - tp);
+      tp = t2;
+    }
+  };
+
+  for (int b = 0; b < NB / IB; ++b) {
+    const int rb0 = b * IB;
+    const int nrows = (MODE == GE) ? NB - rb0 : (MODE == TT ? IB + rb0 + IB : IB + NB);
+    // the part of the stacked panel that is not forwarded by the trailing
+    // update (see panel_item); it does not depend on block b-1 (GE loads
+    // block 0 only; the pivot triangle and TT's new bottom rows are not
+    // touched by earlier blocks), so for b > 0 UG loads it before its
+    // trailing chunks.  lt: thread index within the loading group
+    auto load_rest = [&](int lt) {
+      const bool fwd = b > 0;
+      if (MODE == GE) {
+        if (!fwd) {
+          for (int e0 = lt; e0 < NB * IB; e0 += 8 * FT) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int e = e0 + u * FT;
+              v[u] = e < NB * IB ? __ldcg(at + e % NB + size_t(e / NB) * NB) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int e = e0 + u * FT;
+              if (e < NB * IB) P[e % NB + (e / NB) * PLD] = v[u];
+            }
+          }
+        }
+      } else {
+        constexpr int NBR = (MODE == TT) ? IB : NB;
+        const int rf = (MODE == TT) ? rb0 : 0;
+        const int tot = IB * IB + ((MODE == TT || !fwd) ? NBR * IB : 0);
+        for (int e0 = lt; e0 < tot; e0 += 8 * FT) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * FT;
+            double x = 0.0;
+            if (e < tot) {
+              if (e < IB * IB) {
+                const int r = e % IB, c = e / IB;
+                if (r <= c) x = __ldcg(rt + (rb0 + r) + size_t(rb0 + c) * NB);
+              } else {
+                const int f = e - IB * IB, rr = rf + f % NBR, c = f / NBR;
+                if (MODE == TS || rr <= rb0 + c) x = __ldcg(at + rr + size_t(rb0 + c) * NB);
+              }
+            }
+            v[u] = x;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * FT;
+            if (e < tot) {
+              if (e < IB * IB) {
+                P[e % IB + (e / IB) * PLD] = v[u];
+              } else {
+                const int f = e - IB * IB;
+                P[IB + rf + f % NBR + (f / NBR) * PLD] = v[u];
+              }
+            }
+          }
+        }
+      }
+    };
+    // From block LATE on FG's chain (block b-1 on block b's columns, level-2,
+    // group updates) is longer than UG's trailing chunks: UG then starts them
+    // only once FG's chunks are done, so those run alone on the DMMA pipe.
+    constexpr int LATE = 3;
+    if (!fg) {
+      // UG: the loads, then block b-1's reflectors on the columns right of block b
+      if (b > 0) {
+        if (MODE != GE) load_rest(tid - FT);
+        asm volatile("bar.arrive 4, %0;\n" ::"n"(NT) : "memory");  // panel loaded
+        if (b >= LATE) asm volatile("bar.sync 5, %0;\n" ::"n"(NT) : "memory");
+        panel_trailing<NB, MODE>(at, rt, Vs, Ts, b - 1, warp, lane, P, IB / 8 + warp - FW, 1 << 30, NW - FW);
+      }
+    } else {
+      // FG: block b-1's reflectors on block b's columns (one 8-column chunk
+      // per warp, forwarded into P)
+      if (b > 0) {
+        panel_trailing<NB, MODE>(at, rt, Vs, Ts, b - 1, warp, lane, P, warp, IB / 8, FW);
+        if (b >= LATE) asm volatile("bar.arrive 5, %0;\n" ::"n"(NT) : "memory");
+        asm volatile("bar.sync 4, %0;\n" ::"n"(NT) : "memory");  // FG's chunks and UG's loads are in P
+      } else {
+        load_rest(tid);
+        fsync();
+      }
+      mark(4);
+
+      // rows owned by this thread: t, t + FT, t + 2 FT
+      const int r0w = t, r1w = t + FT, r2w = t + 2 * FT;
+      const bool own0 = r0w < nrows, own1 = r1w < nrows, own2 = MODE != GE && r2w < nrows;  // GE: nrows <= 2 FT
+      auto in_vec = [&](int r, int j) {  // P row r belongs to reflector j's vector part
+        if (MODE == GE) return r > j;
+        if (MODE == TT) return r >= IB && r <= IB + rb0 + j;
+        return r >= IB;
+      };
+      for (int gq = 0; gq < IB / 8; ++gq) {
+        const int c0 = 8 * gq;
+        // ---- level-2 on columns c0..c0+7 (registers: 8 values per owned row)
+        double rv0[8], rv1[8], rv2[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          rv0[c] = own0 ? P[r0w + (c0 + c) * PLD] : 0.0;
+          rv1[c] = own1 ? P[r1w + (c0 + c) * PLD] : 0.0;
+          rv2[c] = own2 ? P[r2w + (c0 + c) * PLD] : 0.0;
+        }
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int j = c0 + jj;
+          double* partj = part + (jj & 1) * (NW * 8);  // double-buffered by column parity
+          double* drowj = drow + (jj & 1) * 8;
+          if (t == j) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) drowj[c] = rv0[c];
+          }
+          const bool iv0 = own0 && in_vec(r0w, j), iv1 = own1 && in_vec(r1w, j), iv2 = own2 && in_vec(r2w, j);
+          double x0 = iv0 ? rv0[jj] : 0.0, x1 = iv1 ? rv1[jj] : 0.0, x2 = iv2 ? rv2[jj] : 0.0;
+          auto reduce8 = [&](double xa, double xb, double xc) {
+            double d[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              d[c] = fma(xb, rv1[c], xa * rv0[c]);
+              if (MODE != GE) d[c] = fma(xc, rv2[c], d[c]);
+            }
+            const bool u4 = lane & 16;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const double snd = u4 ? d[i] : d[i + 4], kp = u4 ? d[i + 4] : d[i];
+              d[i] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+            }
+            const bool u3 = lane & 8;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const double snd = u3 ? d[i] : d[i + 2], kp = u3 ? d[i + 2] : d[i];
+              d[i] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+            }
+            const bool u2 = lane & 4;
+            {
+              const double snd = u2 ? d[0] : d[1], kp = u2 ? d[1] : d[0];
+              d[0] = kp + __shfl_xor_sync(0xffffffffu, snd, 4);
+            }
+            d[0] += __shfl_xor_sync(0xffffffffu, d[0], 2);
+            d[0] += __shfl_xor_sync(0xffffffffu, d[0], 1);
+            if ((lane & 3) == 0)
+              partj[warp * 8 + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = d[0];
+          };
+          const int v = lane & 7;
+          auto sum8 = [&]() {
+            double pw[FW];
+#pragma unroll
+            for (int w = 0; w < FW; ++w) pw[w] = partj[w * 8 + v];
+#pragma unroll
+            for (int h = FW / 2; h >= 1; h >>= 1)
+#pragma unroll
+              for (int w = 0; w < h; ++w) pw[w] += pw[w + h];
+            return pw[0];
+          };
+          reduce8(x0, x1, x2);
+          fsync();
+          const double alpha = drowj[jj];  // row j (written before the barrier)
+          double D = sum8();
+          const double xn2 = __shfl_sync(0xffffffffu, D, jj);
+          const bool rare = __any_sync(0xffffffffu, !(xn2 >= 0x1p-900 && fma(alpha, alpha, xn2) <= 0x1p900) ||
+                                                        !isfinite(D));
+          double tau, scal_d, beta;
+          dlarfg_scalars(alpha, xn2, tau, scal_d, beta);
+          if (__builtin_expect(rare, 0)) {  // scaled path, see panel_item
+            double m = fmax(fmax(iv0 ? fabs(x0) : 0.0, iv1 ? fabs(x1) : 0.0), iv2 ? fabs(x2) : 0.0);
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) sbuf[warp] = m;
+            fsync();
+            double amax = 0.0;
+#pragma unroll
+            for (int w = 0; w < FW; ++w) amax = fmax(amax, sbuf[w]);
+            tau = scal_d = 0.0;
+            beta = alpha;
+            if (amax != 0.0) {
+              const int ex = ilogb(amax);
+              const double xsc = ldexp(1.0, -ex);
+              x0 *= xsc;
+              x1 *= xsc;
+              x2 *= xsc;
+              if (iv0) rv0[jj] = x0;
+              if (iv1) rv1[jj] = x1;
+              if (iv2) rv2[jj] = x2;
+              reduce8(x0, x1, x2);
+              fsync();
+              D = sum8();
+              const double xn2s = __shfl_sync(0xffffffffu, D, jj);
+              if (fabs(alpha) >= ldexp(1.0, ex + 500)) {
+                tau = 2.0;
+                beta = -alpha;
+                scal_d = ldexp(0.5 / alpha, ex);
+              } else {
+                dlarfg_scalars(ldexp(alpha, -ex), xn2s, tau, scal_d, beta);
+                beta = ldexp(beta, ex);
+              }
+            }
+          }
+          const double sv = tau * (drowj[v] + scal_d * D);
+          if (tid == 0) {
+            tau_s[j] = tau;
+            beta_s[j] = beta;
+          }
+          if (tau != 0.0) {
+            double sc[8];
+#pragma unroll
+            for (int c = jj + 1; c < 8; ++c) sc[c] = __shfl_sync(0xffffffffu, sv, c);
+            if (iv0) {
+              const double xs = x0 * scal_d;
+#pragma unroll
+              for (int c = jj + 1; c < 8; ++c) rv0[c] -= sc[c] * xs;
+              rv0[jj] = xs;
+            }
+            if (iv1) {
+              const double xs = x1 * scal_d;
+#pragma unroll
+              for (int c = jj + 1; c < 8; ++c) rv1[c] -= sc[c] * xs;
+              rv1[jj] = xs;
+            }
+            if (iv2) {
+              const double xs = x2 * scal_d;
+#pragma unroll
+              for (int c = jj + 1; c < 8; ++c) rv2[c] -= sc[c] * xs;
+              rv2[jj] = xs;
+            }
+            if (t == j) {
+#pragma unroll
+              for (int c = jj + 1; c < 8; ++c) rv0[c] -= sc[c];
+            }
+          }
+          if (t == j) rv0[jj] = beta;
+          mark(7);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (own0) P[r0w + (c0 + c) * PLD] = rv0[c];
+          if (own1) P[r1w + (c0 + c) * PLD] = rv1[c];
+          if (own2) P[r2w + (c0 + c) * PLD] = rv2[c];
+        }
+        fsync();
+        mark(1);
+        // ---- group update: W = V_g^T [V_g | A_rest] (DMMA, K = rows over the FW warps)
+        if (gq < IB / 8 - 1) {
+          const int ncol = IB - c0 - 8;  // 24, 16, 8
+          const int klo = (MODE == GE) ? (c0 & ~3) : 0;
+          const int khi = (MODE == GE) ? nrows : (MODE == TT ? IB + rb0 + c0 + 8 : nrows);
+          const int ksteps = (khi - klo + 3) >> 2;
+          const int per = (ksteps + FW - 1) / FW;
+          const int ka = klo + 4 * per * warp, kb = min(khi, ka + 4 * per);
+          double acc[4][2];
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
+          if (ka < kb) {
+            const int kbb = ((kb - ka + 3) & ~3) + ka;
+            if (ncol == 24)
+              tn_acc<NB, MODE, 4>(acc, P, c0, ka, kbb, lane);
+            else if (ncol == 16)
+              tn_acc<NB, MODE, 3>(reinterpret_cast<double(&)[3][2]>(acc), P, c0, ka, kbb, lane);
+            else
+              tn_acc<NB, MODE, 2>(reinterpret_cast<double(&)[2][2]>(acc), P, c0, ka, kbb, lane);
+          }
+          {
+            const int r = lane >> 2, c = lane & 3;
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb) {
+              WP[(warp * 8 + r) * LDW + 8 * nb + 2 * c] = acc[nb][0];
+              WP[(warp * 8 + r) * LDW + 8 * nb + 2 * c + 1] = acc[nb][1];
+            }
+          }
+          fsync();
+          if (warp > 0) {
+            for (int e = tid - 32; e < 8 * ncol; e += FT - 32) {
+              const int jr = e / ncol, cc = 8 + e % ncol;
+              double sacc = 0.0;
+#pragma unroll
+              for (int w = 0; w < FW; ++w) sacc += WP[(w * 8 + jr) * LDW + cc];
+              W[jr * LDW + cc] = sacc;
+            }
+          } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int jr = (lane >> 3) + 4 * h, cc = lane & 7;
+              double sacc = 0.0;
+#pragma unroll
+              for (int w = 0; w < FW; ++w) sacc += WP[(w * 8 + jr) * LDW + cc];
+              W[jr * LDW + cc] = sacc;
+            }
+            __syncwarp();
+          }
+          if (warp == 0 && lane < 8) {
+            const int cc = lane;
+            double col[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) col[i] = 0.0;
+#pragma unroll
+            for (int i = 7; i >= 0; --i) {
+              double vv = 0.0;
+              if (i == cc) vv = tau_s[c0 + i];
+              if (i < cc) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int l = i + 1; l < 8; ++l)
+                  if (l <= cc) sacc += W[i * LDW + l] * col[l];
+                vv = -tau_s[c0 + i] * sacc;
+              }
+              col[i] = vv;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) Tg[i + cc * 8] = col[i];
+          }
+          fsync();
+          for (int e = tid; e < 8 * ncol; e += FT) {
+            const int jr = e / ncol, cc = 8 + e % ncol;
+            double sacc = 0.0;
+#pragma unroll
+            for (int l = 0; l < 8; ++l)
+              if (l <= jr) sacc += Tg[l + jr * 8] * W[l * LDW + cc];
+            WP[jr * LDW + cc] = sacc;  // reuse warp-0 slab of WP as the result
+          }
+          fsync();
+          {
+            const int r = lane >> 2, c = lane & 3;
+            const int mlo = klo >> 3, mhi = (khi + 7) >> 3;
+            for (int mb = mlo + warp; mb < mhi; mb += FW) {
+              const int row = 8 * mb + r;
+              double a0 = vmask_p<NB, MODE>(P[row + (c0 + c) * PLD], row, c0 + c);
+              double a1 = vmask_p<NB, MODE>(P[row + (c0 + 4 + c) * PLD], row, c0 + 4 + c);
+              for (int nb = 0; nb < ncol / 8; ++nb) {
+                const int cb = c0 + 8 + 8 * nb;
+                double acc2[2] = {0.0, 0.0};
+                const double b0 = WP[c * LDW + 8 + 8 * nb + r];
+                const double b1 = WP[(4 + c) * LDW + 8 + 8 * nb + r];
+                dmma(acc2, a0, b0);
+                dmma(acc2, a1, b1);
+                if (row < nrows) {
+                  P[8 * mb + r + (cb + 2 * c) * PLD] -= acc2[0];
+                  P[8 * mb + r + (cb + 2 * c + 1) * PLD] -= acc2[1];
+                }
+              }
+            }
+          }
+          fsync();
+          mark(2);
+        }
+      }
+    }
+    csync();  // block b is factored in P; block b-1 is applied to every column right of it
+    // ---- block Gram (compensated), T_b, write-back, staging of V_b and T_b:
+    // all eight warps, as in panel_item
+    {
+      double* Glo = Tp;
+      double* G1 = WP;
+      const int r = lane >> 2, c = lane & 3;
+      for (int u = warp; u < 20; u += NW) {
+        const int pr = u >> 1, half = u & 1;
+        const int mb = pr < 4 ? 0 : (pr < 7 ? 1 : (pr < 9 ? 2 : 3));
+        const int nbb = pr < 4 ? pr : (pr < 7 ? pr - 3 : (pr < 9 ? pr - 5 : 3));
+        const int klo = (MODE == GE) ? 8 * nbb : 0;
+        const int khi = (MODE == TT) ? IB + rb0 + 8 * mb + 8 : (nrows + 3) & ~3;
+        const int mid = klo + (((khi - klo) >> 1) & ~7);
+        const int k0 = half ? mid : klo, k1 = half ? khi : mid;
+        double hi[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, lo[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        for (int k = k0; k < k1; k += 16) {
+          double tt[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int row = k + 4 * h + c;
+            if (k + 4 * h < k1) {
+              const double a = vmask_p<NB, MODE>(P[row + (8 * mb + r) * PLD], row, 8 * mb + r);
+              const double bv = vmask_p<NB, MODE>(P[row + (8 * nbb + r) * PLD], row, 8 * nbb + r);
+              dmma(tt[h >> 1], a, bv);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              double s2, er;
+              two_sum(s2, er, hi[q][e], tt[q][e]);
+              hi[q][e] = s2;
+              lo[q][e] += er;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double s2, er;
+          two_sum(s2, er, hi[0][e], hi[1][e]);
+          const double l2 = er + (lo[0][e] + lo[1][e]);
+          const int idx = (8 * mb + r) + (8 * nbb + 2 * c + e) * IB;
+          if (half == 0) {
+            G[idx] = s2;
+            Glo[idx] = l2;
+          } else {
+            G1[pr * 128 + 2 * lane + e] = s2;
+            G1[pr * 128 + 64 + 2 * lane + e] = l2;
+          }
+        }
+      }
+      csync();
+      for (int e = tid; e < 640; e += NT) {
+        const int pr = e >> 6, w = e & 63, ln = w >> 1;
+        const int mb = pr < 4 ? 0 : (pr < 7 ? 1 : (pr < 9 ? 2 : 3));
+        const int nbb = pr < 4 ? pr : (pr < 7 ? pr - 3 : (pr < 9 ? pr - 5 : 3));
+        const int i = 8 * mb + (ln >> 2), j = 8 * nbb + 2 * (ln & 3) + (w & 1);
+        const int idx = i + j * IB;
+        double s2, er;
+        two_sum(s2, er, G[idx], G1[pr * 128 + w]);
+        const double gv = s2 + (er + (Glo[idx] + G1[pr * 128 + 64 + w]));
+        G[idx] = gv;
+        if (i == j) taut_s[i] = tau_s[i] != 0.0 ? 2.0 / gv : 0.0;
+      }
+    }
+    csync();
+    mark(5);
+    // ---- T_b = U^-1 (dlarft with tau = 2 / v^T v), see panel_item
+    if (warp >= 4) {
+      for (int e = tid - 128; e < 6 * 64; e += NT - 128) {
+        const int k = e >> 6, bi = k < 1 ? 1 : (k < 3 ? 2 : 3), bj = k < 1 ? 0 : (k < 3 ? k - 1 : k - 3);
+        Tp[(bi * 8 + ((e & 63) >> 3)) * IB + bj * 8 + (e & 7)] = 0.0;
+      }
+    }
+    if (warp < 4 && lane < 8) {
+      const int g0 = warp * 8, cc = lane;
+      double col[8], tv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) tv[i] = taut_s[g0 + i];
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        double vv = 0.0;
+        if (i == cc) vv = tv[i];
+        if (i < cc) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int l = i + 1; l < 8; ++l)
+            if (l <= cc) sacc += G[(g0 + i) + (g0 + l) * IB] * col[l];
+          vv = -tv[i] * sacc;
+        }
+        col[i] = vv;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) Tp[(g0 + i) * IB + g0 + cc] = col[i];
+    }
+    csync();
+    double* M = WP;  // scratch, row-major IB x IB
+    if (tid < 128) {
+      const int pb = tid >> 6, e = tid & 63, i = e >> 3, jx = e & 7;
+      const int a0 = 16 * pb, b0 = a0 + 8;
+      double sacc = 0.0;
+#pragma unroll
+      for (int l = 0; l < 8; ++l) sacc += G[(a0 + i) + (b0 + l) * IB] * Tp[(b0 + l) * IB + b0 + jx];
+      M[(a0 + i) * IB + b0 + jx] = sacc;
+    }
+    csync();
+    if (tid < 128) {
+      const int pb = tid >> 6, e = tid & 63, i = e >> 3, jx = e & 7;
+      const int a0 = 16 * pb, b0 = a0 + 8;
+      double sacc = 0.0;
+#pragma unroll
+      for (int l = 0; l < 8; ++l) sacc += Tp[(a0 + i) * IB + a0 + l] * M[(a0 + l) * IB + b0 + jx];
+      Tp[(a0 + i) * IB + b0 + jx] = -sacc;
+    }
+    csync();
+    {
+      const int i = tid >> 4, jx = tid & 15;
+      double sacc = 0.0;
+#pragma unroll
+      for (int l = 0; l < 16; ++l) sacc += G[i + (16 + l) * IB] * Tp[(16 + l) * IB + 16 + jx];
+      M[i * IB + 16 + jx] = sacc;
+    }
+    csync();
+    {
+      const int i = tid >> 4, jx = tid & 15;
+      double sacc = 0.0;
+#pragma unroll
+      for (int l = 0; l < 16; ++l) sacc += Tp[i * IB + l] * M[l * IB + 16 + jx];
+      Tp[i * IB + 16 + jx] = -sacc;
+    }
+    csync();
+    mark(6);
+    // ---- write the block back to HBM, stage V and T for the trailing update
+    for (int e = tid; e < IB * IB; e += NT) {
+      const int i = e % IB, j = e / IB;
+      const double vv = Tp[i * IB + j];
+      Ts[swz(i, j)] = vv;
+      tslot[i + size_t(rb0 + j) * IB] = vv;
+    }
+    csync();  // Vs overwrites Tp / G
+    if (MODE == GE) {
+      for (int c = warp; c < IB; c += NW)
+        for (int r = lane; r < nrows; r += 32) {
+          const double vv = P[r + c * PLD];
+          at[(rb0 + r) + size_t(rb0 + c) * NB] = vv;
+          Vs[swz(rb0 + r, c)] = (r > c) ? vv : (r == c ? 1.0 : 0.0);
+        }
+    } else {
+      const int nb_rows = nrows - IB;
+      for (int c = warp; c < IB; c += NW) {
+        if (lane <= c) rt[(rb0 + lane) + size_t(rb0 + c) * NB] = P[lane + c * PLD];
+        for (int rr = lane; rr < nb_rows; rr += 32) {
+          const bool live = (MODE == TS) || (rr <= rb0 + c);
+          const double vv = live ? P[IB + rr + c * PLD] : 0.0;
+          if (live) at[rr + size_t(rb0 + c) * NB] = vv;
+          Vs[swz(rr, c)] = vv;
+        }
+      }
+    }
+    csync();  // V_b, T_b staged: the groups split again
+    mark(3);
+  }
+}
+
+// The panel item the executor runs: the look-ahead form (TQR_PANEL_NO_LA:
+// panel_item, one phase at a time on all eight warps).
+template <int NB, int MODE>
+__device__ __forceinline__ void panel_run(double* sm, double* at, double* rt, double* tslot, int tid,
+                                          unsigned long long* prof = nullptr) {
+#ifndef TQR_PANEL_NO_LA
+  panel_item_la<NB, MODE>(sm, at, rt, tslot, tid, prof);
+#else
+  panel_item<NB, MODE>(sm, at, rt, tslot, tid, prof);
+#endif
 }
 
 }  // namespace tqrk

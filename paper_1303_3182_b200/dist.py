@@ -210,7 +210,7 @@ def merge_rounds(G):
 class GpuBackend:
     """Local factorization and merges with the libtqr engine."""
 
-    def __init__(self, P, q, nb, device, algo="greedy"):
+    def __init__(self, P, q, nb, device, algo="greedy", family="TT"):
         import torch
 
         from .engine import Plan
@@ -218,7 +218,7 @@ class GpuBackend:
 
         self.torch = torch
         self.P, self.q, self.nb, self.dev = P, q, nb, device
-        self.local_plan = Plan(build_tree(P, q, algo), nb)
+        self.local_plan = Plan(build_tree(P, q, algo, family=family), nb)
         self.tiles, self.tg, self.te = self.local_plan.alloc(device)
         self._merges = {}  # G stacked R blocks -> (plan, tiles, tg, te)
         self._merge_setup(2)

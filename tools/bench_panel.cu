@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(NTP, 1) k_pan(double* tiles, double* tslot, in
   }
   setmaxnreg_inc<232>();
   for (int r = 0; r < reps; ++r) {
-    panel_item<NB, MODE>(sm, at, MODE == GE ? nullptr : rt, tslot + size_t(blockIdx.x) * IB * NB, threadIdx.x,
+    panel_run<NB, MODE>(sm, at, MODE == GE ? nullptr : rt, tslot + size_t(blockIdx.x) * IB * NB, threadIdx.x,
                          blockIdx.x == 0 ? prof : nullptr);
     csync();
   }

@@ -1,7 +1,9 @@
 #!/bin/bash
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
-timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 4 > gpurun_out/s4.c3tt.json 2>gpurun_out/s4.c3tt.err
-timeout 600 python bench.py --family TS --no-cpu-baseline --no-e2e --steps 4 > gpurun_out/s4.c3ts.json 2>gpurun_out/s4.c3ts.err
-timeout 600 python bench.py --config c4 --family TS --no-cpu-baseline --no-e2e --steps 4 > gpurun_out/s4.c4ts.json 2>gpurun_out/s4.c4ts.err
-timeout 600 python tools/item_trace.py --config c3 --family TS --out gpurun_out/s4.trace_c3ts.json > gpurun_out/s4.trace_c3ts.log 2>&1
+timeout 60 ./tools/bench_panel_la > gpurun_out/bp_la.txt 2>&1; echo "exit $?" >> gpurun_out/bp_la.txt
+export TQR_LIB_PATH=$PWD/paper_1303_3182_b200/libtqr_la.so
+timeout 600 python -m pytest tests/test_numeric_gpu.py -m gpu -x -q > gpurun_out/la.pytest.log 2>&1; echo "exit $?" >> gpurun_out/la.pytest.log
+for c in c4 c3 c5; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 4 > gpurun_out/la.$c.json 2>gpurun_out/la.$c.err
+done
 echo done

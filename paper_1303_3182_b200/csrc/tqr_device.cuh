@@ -56,6 +56,23 @@ __device__ unsigned long long g_uprof[32];
 #define UPROF_DECL_V(v)
 #endif
 
+// Update-kernel accumulation choices (in-executor A/B at C3 / C5, one B200):
+//  * the T multiply's odd row halves in a second DMMA chain (half the
+//    dependent-DMMA depth): C3 256.5 -> 253.5 ms (TQR_NO_T_SPLIT_H restores one);
+//  * X -= V W accumulates straight into X instead of from zero with one
+//    final subtraction: 64 DADDs and 8 live registers less per reflector
+//    block, C3 253.5 -> 247.8 ms, C5 931 -> 912 ms.  The update's rounding is
+//    then ~32 FMA roundings at |X| per block instead of one; measured at
+//    n = 16384: ||A - QR|| / ||A|| 5.07e-15 -> 5.93e-15, ||Q^T Q - I||_F
+//    6.08e-13 unchanged (Q's orthogonality is set by V and T, not by the
+//    updates).  TQR_NO_DIRECT_ACC restores the from-zero form.
+#if !defined(TQR_NO_T_SPLIT_H) && !defined(TQR_T_SPLIT_H)
+#define TQR_T_SPLIT_H
+#endif
+#if !defined(TQR_NO_DIRECT_ACC) && !defined(TQR_DIRECT_ACC)
+#define TQR_DIRECT_ACC
+#endif
+
 constexpr int NT = 256;  // compute threads per CTA (8 warps)
 constexpr int NW = 8;
 constexpr int TLD = 40;  // ld of the staged pivot rows (IB + 8: conflict-free 16-byte reads)
@@ -342,6 +359,11 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
   double wt[4][2], wtl[4][2];
 #pragma unroll
   for (int nb = KA; nb < KB; ++nb) wt[nb][0] = wt[nb][1] = wtl[nb][0] = wtl[nb][1] = 0.0;
+#ifdef TQR_T_SPLIT_H
+  double wt2[4][2];  // the odd row halves' chain
+#pragma unroll
+  for (int nb = KA; nb < KB; ++nb) wt2[nb][0] = wt2[nb][1] = 0.0;
+#endif
 #pragma unroll
   for (int kb = KA; kb < KB; ++kb)
 #pragma unroll
@@ -355,9 +377,22 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
           if constexpr (COMP)
             dmma_comp(wt[nb], wtl[nb], w[kb][h], tb[h][kb][nb]);
           else
+#ifdef TQR_T_SPLIT_H
+            dmma(h ? wt2[nb] : wt[nb], w[kb][h], tb[h][kb][nb]);
+#else
             dmma(wt[nb], w[kb][h], tb[h][kb][nb]);
 #endif
+#endif
         }
+#ifdef TQR_T_SPLIT_H
+  if constexpr (!COMP) {
+#pragma unroll
+    for (int nb = KA; nb < KB; ++nb) {
+      wt[nb][0] += wt2[nb][0];
+      wt[nb][1] += wt2[nb][1];
+    }
+  }
+#endif
   if constexpr (COMP) {
 #pragma unroll
     for (int nb = KA; nb < KB; ++nb) {
@@ -376,8 +411,8 @@ __device__ __forceinline__ void warp_apply_k(double (&x)[NB / 8][2], int rb0, in
   }
   UPROF_MARK_V(14, _tq);
   UPROF_MARK_DEP(11, _tq, wt[KB - 1][1]);
-  // X -= W^T V^T ; per 32-row block the product is accumulated from zero and
-  // subtracted from X once (LAPACK-like rounding of the large operand)
+  // X -= W^T V^T, accumulated straight into X (TQR_NO_DIRECT_ACC: per 32-row
+  // block from zero, subtracted from X once)
 #pragma unroll
   for (int rb = 0; rb < NB / IB; ++rb) {
     if (rb >= RBL && rb < RBH && rb >= rb0 && rb < rb1) {

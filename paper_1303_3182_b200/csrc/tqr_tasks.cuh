@@ -1029,16 +1029,11 @@ __device__ void panel_item_la(double* sm, double* at /*GE: tile; TT/TS: bottom t
         }
       }
     };
-    // From block LATE on FG's chain (block b-1 on block b's columns, level-2,
-    // group updates) is longer than UG's trailing chunks: UG then starts them
-    // only once FG's chunks are done, so those run alone on the DMMA pipe.
-    constexpr int LATE = 3;
     if (!fg) {
       // UG: the loads, then block b-1's reflectors on the columns right of block b
       if (b > 0) {
         if (MODE != GE) load_rest(tid - FT);
         asm volatile("bar.arrive 4, %0;\n" ::"n"(NT) : "memory");  // panel loaded
-        if (b >= LATE) asm volatile("bar.sync 5, %0;\n" ::"n"(NT) : "memory");
         panel_trailing<NB, MODE>(at, rt, Vs, Ts, b - 1, warp, lane, P, IB / 8 + warp - FW, 1 << 30, NW - FW);
       }
     } else {
@@ -1046,7 +1041,6 @@ __device__ void panel_item_la(double* sm, double* at /*GE: tile; TT/TS: bottom t
       // per warp, forwarded into P)
       if (b > 0) {
         panel_trailing<NB, MODE>(at, rt, Vs, Ts, b - 1, warp, lane, P, warp, IB / 8, FW);
-        if (b >= LATE) asm volatile("bar.arrive 5, %0;\n" ::"n"(NT) : "memory");
         asm volatile("bar.sync 4, %0;\n" ::"n"(NT) : "memory");  // FG's chunks and UG's loads are in P
       } else {
         load_rest(tid);

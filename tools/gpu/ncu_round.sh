@@ -1,7 +1,7 @@
 #!/bin/bash
 # ncu captures (round 2): C3 executor, update + panel microbenchmarks, launch list
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
-T=ncu2
+T=${1:-ncu2}
 NCU="ncu --set full --clock-control none --import-source on"
 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/$T.c3plain.json 2>&1 &&
 timeout 1500 $NCU -k regex:exec_kernel -s 3 -c 1 -o gpurun_out/$T.c3 -f \

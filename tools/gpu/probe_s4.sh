@@ -1,10 +1,7 @@
 #!/bin/bash
-# in-executor A/B of library variants (libtqr.so = product; libtqr_v*.so = ablations)
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
-for v in "" _v1 _v2 _v3; do
-  [ -f paper_1303_3182_b200/libtqr$v.so ] || continue
-  for c in c3 c4 c5; do
-    TQR_LIB_PATH=$PWD/paper_1303_3182_b200/libtqr$v.so timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 4 > gpurun_out/ab$v.$c.json 2>/dev/null
-  done
-done
+timeout 600 python tools/item_trace.py --config c3 --stream --out gpurun_out/s4.trace_c3_stream.json > gpurun_out/s4.trace_c3_stream.log 2>&1
+timeout 600 python tools/item_trace.py --config c3 --out gpurun_out/s4.trace_c3.json > gpurun_out/s4.trace_c3.log 2>&1
+timeout 600 python tools/item_trace.py --config c5 --out gpurun_out/s4.trace_c5.json > gpurun_out/s4.trace_c5.log 2>&1
+timeout 600 python tools/item_trace.py --config c4 --out gpurun_out/s4.trace_c4.json > gpurun_out/s4.trace_c4.log 2>&1
 echo done

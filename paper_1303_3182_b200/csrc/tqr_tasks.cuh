@@ -40,7 +40,8 @@ struct Smem {
   static constexpr int L_W = P_T + TS, L_TG = L_W + 8 * LDW, L_PART = L_TG + 64, L_DROW = L_PART + 2 * NW * 8;
   static constexpr int L_SBUF = L_DROW + 16, L_SC = L_SBUF + 8, L_WP = L_SC + 3 * IB + 8;
   static constexpr int L_V = L_WP + FW * 8 * LDW, L_G = L_V + 256, L_TT = L_G + TS;
-  static constexpr int L_END = (L_V + VS > L_TT + TS) ? L_V + VS : L_TT + TS;
+  static constexpr int L_G1 = L_TT + TS;  // second halves of the Gram units: [pair][hi 64 | lo 64]
+  static constexpr int L_END = (L_V + VS > L_G1 + 1280) ? L_V + VS : L_G1 + 1280;
   static_assert(L_V % 2 == 0, "16-byte aligned staging");
   static constexpr int END0 = U_END > P_END ? U_END : P_END;
 #ifndef TQR_PANEL_NO_LA
@@ -951,10 +952,61 @@ __device__ void panel_item_la(double* sm, double* at /*GE: tile; TT/TS: bottom t
   double* tau_s = sm + S::L_SC;
   double* taut_s = tau_s + IB;
   double* beta_s = tau_s + 2 * IB;
-  double* WP = sm + S::L_WP;  // [FW][8][LDW] partial W; Gram halves / T scratch (runs into Vs, dead then)
+  double* WP = sm + S::L_WP;  // [FW][8][LDW] partial W; T scratch
   double* Vs = sm + S::L_V;
   double* G = sm + S::L_G;    // G[l + j*IB] = v_l . v_j   (aliases Vs)
   double* Tp = sm + S::L_TT;  // T_b plain, row-major      (aliases Vs)
+  double* G1 = sm + S::L_G1;  // Gram units' second halves (aliases Vs)
+  double* Glo = Tp;           // first halves' low parts (Tp is first written after the combine)
+  // One unit of the compensated block Gram (see panel_item): half `half` of
+  // the row range of the 8x8 block pair pr.  Pairs of column groups 0..2 only
+  // need those groups' reflectors, which are final once group 2's level-2
+  // sweep is done: UG computes them while FG finishes the block.
+  auto gram_unit = [&](int pr, int half, int rb0, int nrows) {
+    const int r = lane >> 2, c = lane & 3;
+    const int mb = pr < 4 ? 0 : (pr < 7 ? 1 : (pr < 9 ? 2 : 3));
+    const int nbb = pr < 4 ? pr : (pr < 7 ? pr - 3 : (pr < 9 ? pr - 5 : 3));
+    const int klo = (MODE == GE) ? 8 * nbb : 0;
+    const int khi = (MODE == TT) ? IB + rb0 + 8 * mb + 8 : (nrows + 3) & ~3;
+    const int mid = klo + (((khi - klo) >> 1) & ~7);
+    const int k0 = half ? mid : klo, k1 = half ? khi : mid;
+    double hi[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, lo[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int k = k0; k < k1; k += 16) {
+      double tt[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int row = k + 4 * h + c;
+        if (k + 4 * h < k1) {
+          const double a = vmask_p<NB, MODE>(P[row + (8 * mb + r) * PLD], row, 8 * mb + r);
+          const double bv = vmask_p<NB, MODE>(P[row + (8 * nbb + r) * PLD], row, 8 * nbb + r);
+          dmma(tt[h >> 1], a, bv);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double s2, er;
+          two_sum(s2, er, hi[q][e], tt[q][e]);
+          hi[q][e] = s2;
+          lo[q][e] += er;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double s2, er;
+      two_sum(s2, er, hi[0][e], hi[1][e]);
+      const double l2 = er + (lo[0][e] + lo[1][e]);
+      const int idx = (8 * mb + r) + (8 * nbb + 2 * c + e) * IB;
+      if (half == 0) {
+        G[idx] = s2;
+        Glo[idx] = l2;
+      } else {
+        G1[pr * 128 + 2 * lane + e] = s2;
+        G1[pr * 128 + 64 + 2 * lane + e] = l2;
+      }
+    }
+  };
   const int t = tid;
   const bool fg = warp < FW;
   auto fsync = [&]() { asm volatile("bar.sync 3, %0;\n" ::"n"(FT) : "memory"); };
@@ -1035,6 +1087,13 @@ __device__ void panel_item_la(double* sm, double* at /*GE: tile; TT/TS: bottom t
         if (MODE != GE) load_rest(tid - FT);
         asm volatile("bar.arrive 4, %0;\n" ::"n"(NT) : "memory");  // panel loaded
         panel_trailing<NB, MODE>(at, rt, Vs, Ts, b - 1, warp, lane, P, IB / 8 + warp - FW, 1 << 30, NW - FW);
+      }
+      // the Gram pairs of column groups 0..2 (V_{b-1} staged in Vs is dead:
+      // FG's chunks ended before its level-2 sweep, UG's just now)
+      asm volatile("bar.sync 5, %0;\n" ::"n"(NT) : "memory");  // groups 0..2 are final in P
+      for (int u = warp - FW; u < 12; u += NW - FW) {
+        const int e6 = u >> 1;
+        gram_unit(e6 < 3 ? e6 : (e6 < 5 ? e6 + 1 : 7), u & 1, rb0, nrows);
       }
     } else {
       // FG: block b-1's reflectors on block b's columns (one 8-column chunk
@@ -1202,6 +1261,7 @@ __device__ void panel_item_la(double* sm, double* at /*GE: tile; TT/TS: bottom t
           if (own2) P[r2w + (c0 + c) * PLD] = rv2[c];
         }
         fsync();
+        if (gq == 2) asm volatile("bar.arrive 5, %0;\n" ::"n"(NT) : "memory");  // groups 0..2 final: UG's Gram pairs
         mark(1);
         // ---- group update: W = V_g^T [V_g | A_rest] (DMMA, K = rows over the FW warps)
         if (gq < IB / 8 - 1) {
@@ -1312,53 +1372,10 @@ __device__ void panel_item_la(double* sm, double* at /*GE: tile; TT/TS: bottom t
     // ---- block Gram (compensated), T_b, write-back, staging of V_b and T_b:
     // all eight warps, as in panel_item
     {
-      double* Glo = Tp;
-      double* G1 = WP;
-      const int r = lane >> 2, c = lane & 3;
-      for (int u = warp; u < 20; u += NW) {
-        const int pr = u >> 1, half = u & 1;
-        const int mb = pr < 4 ? 0 : (pr < 7 ? 1 : (pr < 9 ? 2 : 3));
-        const int nbb = pr < 4 ? pr : (pr < 7 ? pr - 3 : (pr < 9 ? pr - 5 : 3));
-        const int klo = (MODE == GE) ? 8 * nbb : 0;
-        const int khi = (MODE == TT) ? IB + rb0 + 8 * mb + 8 : (nrows + 3) & ~3;
-        const int mid = klo + (((khi - klo) >> 1) & ~7);
-        const int k0 = half ? mid : klo, k1 = half ? khi : mid;
-        double hi[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, lo[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-        for (int k = k0; k < k1; k += 16) {
-          double tt[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const int row = k + 4 * h + c;
-            if (k + 4 * h < k1) {
-              const double a = vmask_p<NB, MODE>(P[row + (8 * mb + r) * PLD], row, 8 * mb + r);
-              const double bv = vmask_p<NB, MODE>(P[row + (8 * nbb + r) * PLD], row, 8 * nbb + r);
-              dmma(tt[h >> 1], a, bv);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              double s2, er;
-              two_sum(s2, er, hi[q][e], tt[q][e]);
-              hi[q][e] = s2;
-              lo[q][e] += er;
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          double s2, er;
-          two_sum(s2, er, hi[0][e], hi[1][e]);
-          const double l2 = er + (lo[0][e] + lo[1][e]);
-          const int idx = (8 * mb + r) + (8 * nbb + 2 * c + e) * IB;
-          if (half == 0) {
-            G[idx] = s2;
-            Glo[idx] = l2;
-          } else {
-            G1[pr * 128 + 2 * lane + e] = s2;
-            G1[pr * 128 + 64 + 2 * lane + e] = l2;
-          }
-        }
+      // the pairs with column group 3 (two halves each: one unit per warp)
+      {
+        const int l4 = warp >> 1;
+        gram_unit(l4 == 0 ? 3 : (l4 == 1 ? 6 : (l4 == 2 ? 8 : 9)), warp & 1, rb0, nrows);
       }
       csync();
       for (int e = tid; e < 640; e += NT) {

@@ -1,7 +1,8 @@
 #!/bin/bash
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
-timeout 600 python tools/item_trace.py --config c3 --stream --out gpurun_out/s4.trace_c3_stream.json > gpurun_out/s4.trace_c3_stream.log 2>&1
-timeout 600 python tools/item_trace.py --config c3 --out gpurun_out/s4.trace_c3.json > gpurun_out/s4.trace_c3.log 2>&1
-timeout 600 python tools/item_trace.py --config c5 --out gpurun_out/s4.trace_c5.json > gpurun_out/s4.trace_c5.log 2>&1
-timeout 600 python tools/item_trace.py --config c4 --out gpurun_out/s4.trace_c4.json > gpurun_out/s4.trace_c4.log 2>&1
+timeout 60 ./tools/bench_panel > gpurun_out/bp_la2.txt 2>&1; echo "exit $?" >> gpurun_out/bp_la2.txt
+timeout 600 python -m pytest tests/test_numeric_gpu.py -m gpu -x -q > gpurun_out/la.pytest.log 2>&1; echo "exit $?" >> gpurun_out/la.pytest.log
+for c in c4 c3 c5; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 4 > gpurun_out/la.$c.json 2>gpurun_out/la.$c.err
+done
 echo done

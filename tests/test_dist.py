@@ -228,6 +228,24 @@ def test_gpu_streamed_local_factorization_matches_device_path():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("family", ["TT", "TS"])
+def test_gpu_backend_local_family(family):
+    """GpuBackend's local tree in either kernel family (tiledag family= of
+    build_tree; TS: lazily triangularized pivots, TSQRT/TSMQR for rows that
+    never were pivots): the same R up to row signs."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    P, q, nb = 16, 4, 64
+    A = _matrix(P, q, nb, seed=17)
+    be = dist.GpuBackend(P, q, nb, torch.device("cuda"), family=family)
+    assert be.local_plan.build.family == family
+    rb = be.factor_local(torch.from_numpy(A).cuda())
+    R = row_sign_normalize(be.r_matrix(rb).cpu().numpy())
+    Rref = row_sign_normalize(np.linalg.qr(A, mode="r"))
+    assert np.linalg.norm(R - Rref) <= 1e-11 * np.linalg.norm(A)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("G,p,q,nb,merge", [(2, 8, 2, 64, "binary"), (4, 16, 4, 64, "binary"), (4, 16, 2, 256, "binary"),
                                             (4, 16, 4, 64, "gather"), (8, 16, 2, 256, "gather")])
 def test_gpu_emulated_apply_q(G, p, q, nb, merge):

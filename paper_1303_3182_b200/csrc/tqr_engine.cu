@@ -263,12 +263,18 @@ bool cp_order(std::vector<Item>& items, std::vector<int32_t>& preds, int workers
   const bool throughput = n_upd >= 2000 * size_t(workers);
   const double panel = env_cost("TQR_COST_PANEL", throughput ? 3.0 : 8.0);
   for (size_t v = 0; v < n; ++v) w[v] = item_cost(items[v].kind, nb, panel);
-  // simulated durations: the panel cost may differ from the one the
-  // priorities use (TQR_SIM_PANEL: panel items' duration multiplier)
-  static const double sim_panel = env_cost("TQR_SIM_PANEL", 1.0);
+  // simulated durations: panels at their measured length (GEQRT 350 us,
+  // TTQRT 335 us, TSQRT 433 us against 47 us for an update slab: the
+  // critical-path weight 8), whatever weight the priorities use.  With the
+  // light priority weight of the throughput-bound plans the simulated panels
+  // used to end three times too early, and the order then expects their
+  // successors early: C3 end to end 256.8 -> 250.8 ms (host A streamed in,
+  // tools/gpu/e2e_knobs.sh), resident unchanged.  TQR_SIM_PANEL overrides
+  // the simulated panel weight.
+  static const double sim_panel = env_cost("TQR_SIM_PANEL", 8.0);
   std::vector<double> wd(w);
   for (size_t v = 0; v < n; ++v)
-    if (items[v].kind <= tqr::TSQRT) wd[v] = w[v] * sim_panel;
+    if (items[v].kind <= tqr::TSQRT) wd[v] = item_cost(items[v].kind, nb, std::max(panel, sim_panel));
   for (size_t v = n; v-- > 0;) {  // items are in a topological order already
     double best = 0.0;
     for (int32_t k = nsucc[v]; k < nsucc[v + 1]; ++k) best = std::max(best, prio[size_t(succ[size_t(k)])]);
@@ -564,7 +570,8 @@ int tqr_plan_create_io(const tqr_build* hb, int nb, int ib, int io, tqr_plan** o
         // modeled arrival (item-cost units, ~50 GB/s host link; an update
         // slab item ~ 54 us at nb=256), indexed by flag (j-1)*anch + c
         const double unit_s = 54e-6 * (double(nb) / 256.0) * (double(nb) / 256.0);
-        // modeled pinned H2D rate (measured ~47.7 GB/s on the pool's boxes);
+        // modeled pinned H2D rate (measured 47.7-55.5 GB/s on the pool's
+        // boxes; modeling 56 instead: C3 end to end -0.7 ms, C4 +0.7 ms);
         // TQR_H2D_GBS overrides
         static const double h2d_bps = env_cost("TQR_H2D_GBS", 48.0) * 1e9;
         unit_release.assign(size_t(b.q) * P->anch, 0.0);

@@ -1,4 +1,5 @@
 #!/bin/bash
+# (pre-session-4 semantics: TQR_SIM_PANEL was a multiplier; it is now an absolute weight)
 # C4 sweep of the simulated panel duration (TQR_SIM_PANEL, multiplier of the
 # panel weight in the list-schedule simulation) at the default priority weight
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out

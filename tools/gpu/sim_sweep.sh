@@ -1,4 +1,5 @@
 #!/bin/bash
+# (pre-session-4 semantics: TQR_SIM_PANEL was a multiplier; it is now an absolute weight)
 # C3: simulated panel duration (TQR_SIM_PANEL x priority weight) sweep
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
 for s in 1 1.5 2 2.8; do

@@ -569,7 +569,8 @@ int tqr_plan_create_io(const tqr_build* hb, int nb, int ib, int io, tqr_plan** o
           for (int c = 0; c < P->anch; ++c) unit(j, c);
         // modeled arrival (item-cost units, ~50 GB/s host link; an update
         // slab item ~ 54 us at nb=256), indexed by flag (j-1)*anch + c
-        const double unit_s = 54e-6 * (double(nb) / 256.0) * (double(nb) / 256.0);
+        static const double unit_us = env_cost("TQR_UNIT_US", 54.0);
+        const double unit_s = unit_us * 1e-6 * (double(nb) / 256.0) * (double(nb) / 256.0);
         // modeled pinned H2D rate (measured 47.7-55.5 GB/s on the pool's
         // boxes; modeling 56 instead: C3 end to end -0.7 ms, C4 +0.7 ms);
         // TQR_H2D_GBS overrides

@@ -366,6 +366,12 @@ __global__ void __launch_bounds__(NTP, 1) exec_kernel(ExecParams P) {
             const int pr = P.preds[X.pred_lo + t];
             if (pr != it && ld_acquire(P.done + pr) == 0) ok = 0;
           }
+          // a PACK item is ready once its arrival unit has landed (otherwise
+          // the CTA would sit in it waiting for the host copy while ready
+          // work queues behind: the modeled arrival times are only a model)
+          if (X.kind == tqr::PACK && lane == 0 &&
+              ld_acquire_sys(P.arrive + (X.j - 1) * P.anch + (X.i - 1) / P.acr) == 0)
+            ok = 0;
           return __all_sync(0xffffffffu, ok) != 0;
         };
         int cur = nx, nxt;
